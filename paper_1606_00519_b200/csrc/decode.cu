@@ -1,0 +1,644 @@
+// decode.cu — sm_100a kernels of the Gompresso decompression hot path and their C-ABI launchers.
+//
+//   huff_decode_kernel  Gompresso/Bit, one CTA per data block:
+//       a1 block-table entry checks; a2 CTA-wide exclusive scans of the sub-block bit sizes and literal counts
+//       (P:48-50); a3 canonical code lengths -> two 2^LB-entry lookup tables in shared memory
+//       (P:73-77); a4 one thread per sub-block decodes its bitstream with one table lookup per
+//       symbol into Byte-format records and literals in the workspace token buffer.
+//   lz77_kernel<STRAT>  one warp per data block, one sequence per lane: a5 read 32
+//       records + one packed warp exclusive scan giving both prefix sums; a6 literal
+//       copy; a7 back-references by Dependency Elimination (one round), Multi-Round Resolution
+//       (Fig. alg:mrr, HWM reading R1) or Sequential Copying. For Gompresso/Byte the
+//       same kernel reads the records straight from the file (a8, single pass).
+//   a9 completion: first-error-wins error word and optional MRR statistics in the workspace.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "format.hpp"
+#include "gomp.h"
+
+#define GOMP_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace gomp {
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr int kLz77Warps = 4;        // warps (= data blocks) per CTA of the LZ77 kernel
+constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
+
+// workspace layout (kWsHeaderBytes = 1024): [0,16) gomp_error; [64, 64+8*67) gomp_stats; token buffer at 1024
+constexpr size_t kWsStatsOff = 64;
+
+struct Args {
+  const uint8_t* src;     // compressed file (device)
+  uint8_t* dst;           // output of block first_block
+  uint8_t* tokens;        // Bit: token buffer, block i of the range at tokens + i * tok_stride
+  uint8_t* ws;            // workspace base (error word, stats)
+  uint64_t total, file_len, payload_base, tok_stride;
+  uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, lut_bits, max_tok;
+  uint32_t n_sub_total, nb_total;
+};
+
+// ------------------------------------------------------------------ completion: error word (a9)
+__device__ __forceinline__ void report(const Args& a, int status, uint32_t block, uint64_t detail) {
+  gomp_error* e = reinterpret_cast<gomp_error*>(a.ws);
+  if (atomicCAS(&e->status, 0, status) == 0) {
+    e->block = block;
+    e->detail = detail;
+  }
+}
+__device__ __forceinline__ unsigned long long* stats_ptr(const Args& a) {
+  return reinterpret_cast<unsigned long long*>(a.ws + kWsStatsOff);
+}
+
+__device__ __forceinline__ BlockEntry load_entry(const uint8_t* src, uint32_t b, uint32_t lane) {
+  const uint32_t* te = reinterpret_cast<const uint32_t*>(src + kHeaderBytes + uint64_t(kBlockEntryBytes) * b);
+  uint32_t w = lane < 8 ? __ldg(te + lane) : 0u;
+  BlockEntry e;
+  e.payload_off = uint64_t(__shfl_sync(FULL, w, 0)) | uint64_t(__shfl_sync(FULL, w, 1)) << 32;
+  e.payload_len = __shfl_sync(FULL, w, 2);
+  e.n_seq = __shfl_sync(FULL, w, 3);
+  e.n_lit = __shfl_sync(FULL, w, 4);
+  e.sub_first = __shfl_sync(FULL, w, 5);
+  e.S = __shfl_sync(FULL, w, 6);
+  e.n_sub = __shfl_sync(FULL, w, 7);
+  return e;
+}
+
+__device__ __forceinline__ uint32_t block_ulen(const Args& a, uint32_t b) {
+  const uint64_t off = uint64_t(b) * a.block_size;
+  const uint64_t rem = a.total - off;
+  return uint32_t(rem < a.block_size ? rem : a.block_size);
+}
+
+__device__ __forceinline__ bool payload_ok(const Args& a, const BlockEntry& e) {
+  return e.payload_off % 16 == 0 && e.payload_len % 16 == 0 && e.payload_off >= a.payload_base &&
+         e.payload_off + e.payload_len <= a.file_len - kTrailerBytes;
+}
+
+// ------------------------------------------------------------------ DEFLATE symbol tables (RFC 1951 §3.2.5)
+__constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                        31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_len_extra[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2,
+                                        2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dist_base[30] = {1,    2,    3,    4,    5,    7,    9,    13,    17,    25,
+                                         33,   49,   65,   97,   129,  193,  257,  385,   513,   769,
+                                         1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6,
+                                         6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+
+// LUT entry: bits 0-3 code length (0 = not resolvable by the table: long code or invalid), 4-5 kind,
+// litlen: literal byte or length base in bits 8-16, extra-bit count in 17-19; dist: base 8-23, extra 24-27.
+enum : uint32_t { K_LIT = 0, K_LEN = 1, K_EOB = 2, K_BAD = 3 };
+__device__ __forceinline__ uint32_t ll_entry(uint32_t sym, uint32_t len) {
+  if (sym < 256) return len | (K_LIT << 4) | (sym << 8);
+  if (sym == 256) return len | (K_EOB << 4);
+  if (sym <= 285) {
+    const uint32_t i = sym - 257;
+    return len | (K_LEN << 4) | (uint32_t(c_len_base[i]) << 8) | (uint32_t(c_len_extra[i]) << 17);
+  }
+  return K_BAD << 4;
+}
+__device__ __forceinline__ uint32_t d_entry(uint32_t sym, uint32_t len) {
+  if (sym < 30) return len | (uint32_t(c_dist_base[sym]) << 8) | (uint32_t(c_dist_extra[sym]) << 24);
+  return K_BAD << 4;
+}
+
+struct CanonTab {        // canonical code description of one table (RFC 1951 §3.2.2)
+  uint16_t count[16];
+  uint16_t first[16];
+  uint16_t index[16];
+  uint16_t running[16];
+};
+
+struct HuffSmem {
+  CanonTab tab[2];
+  uint16_t sorted_ll[288];
+  uint16_t sorted_d[32];
+  uint8_t lens[320];     // 286 litlen + 30 dist code lengths
+  uint32_t bad;
+  uint32_t wlits[8];
+  uint64_t wbits[8];
+  uint64_t carry_bits;
+  uint32_t carry_lits;
+};
+
+// canonical walk for codes longer than the table index (cwl > lut_bits): bits are taken LSB-first from buf
+__device__ int canon_slow(uint64_t buf, const CanonTab& t, const uint16_t* sorted, uint32_t* len_out) {
+  int code = 0, first = 0, index = 0;
+  for (int l = 1; l <= 15; ++l) {
+    code |= int((buf >> (l - 1)) & 1u);
+    const int cnt = t.count[l];
+    if (code - first < cnt) {
+      *len_out = uint32_t(l);
+      return sorted[index + code - first];
+    }
+    index += cnt;
+    first += cnt;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL, v, d);
+    if (lane >= uint32_t(d)) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t t = __shfl_up_sync(FULL, v, d);
+    if (lane >= uint32_t(d)) v += t;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
+__global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
+  uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
+  const uint32_t lut_n = 1u << a.lut_bits;
+  uint32_t* lut_d = lut_ll + lut_n;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
+  const BlockEntry e = load_entry(a.src, b, lane);
+  const uint32_t ulen = block_ulen(a, b);
+
+  // a1: table checks (uniform across the CTA)
+  bool ok = payload_ok(a, e) && e.payload_len >= kTreeBytes && e.S >= 1 &&
+            e.n_sub == (e.n_seq + e.S - 1) / e.S && uint64_t(e.sub_first) + e.n_sub <= a.n_sub_total &&
+            4ull * e.n_seq + e.n_lit <= a.max_tok && e.n_lit <= ulen && e.n_seq <= ulen;
+  if (!ok) {
+    if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
+    return;
+  }
+  const uint8_t* pl = a.src + e.payload_off;
+  if (tid == 0) { sm.bad = 0; sm.carry_bits = 0; sm.carry_lits = 0; }
+  if (tid < 32) {
+    for (int t = 0; t < 2; ++t) {
+      if (lane < 16) { sm.tab[t].count[lane] = 0; sm.tab[t].running[lane] = 0; }
+    }
+  }
+  // unpack the 286 + 30 nibble code lengths (FORMAT.md §3)
+  for (uint32_t s = tid; s < 316; s += blockDim.x) {
+    const uint32_t byte = s < 286 ? pl[s >> 1] : pl[143 + ((s - 286) >> 1)];
+    const uint32_t nib = s < 286 ? (s & 1) : ((s - 286) & 1);
+    sm.lens[s] = uint8_t((byte >> (4 * nib)) & 15u);
+  }
+  __syncthreads();
+  // a3: canonical tables, warp 0 (count / first / index / sorted symbols via __match_any_sync ranks)
+  if (warp == 0) {
+    uint32_t badl = 0;
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t n = t ? 30 : 286, off = t ? 286 : 0;
+      CanonTab& T = sm.tab[t];
+      for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t s = base + lane;
+        const uint32_t l = s < n ? sm.lens[off + s] : 0u;
+        badl |= l > a.cwl;
+        const uint32_t m = __match_any_sync(FULL, l);
+        if (l && (m & ((1u << lane) - 1)) == 0) T.count[l] += __popc(m);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        int left = 1;
+        uint32_t first = 0, index = 0;
+        T.count[0] = 0;
+        for (int l = 1; l <= 15; ++l) {
+          left = (left << 1) - T.count[l];
+          if (left < 0) badl = 1;                        // over-subscribed code set
+          first = l == 1 ? 0u : (first + T.count[l - 1]) << 1;
+          T.first[l] = uint16_t(first);
+          T.index[l] = uint16_t(index);
+          index += T.count[l];
+        }
+      }
+      __syncwarp();
+      uint16_t* sorted = t ? sm.sorted_d : sm.sorted_ll;
+      for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t s = base + lane;
+        const uint32_t l = s < n ? sm.lens[off + s] : 0u;
+        const uint32_t m = __match_any_sync(FULL, l);
+        const uint32_t rank = __popc(m & ((1u << lane) - 1));
+        if (l && l <= 15) sorted[T.index[l] + T.running[l] + rank] = uint16_t(s);
+        __syncwarp();
+        if (l && rank == 0) T.running[l] += __popc(m);
+        __syncwarp();
+      }
+    }
+    badl |= (pl[158] | pl[159]) != 0;
+    badl = __any_sync(FULL, badl);
+    if (lane == 0 && badl) sm.bad = 1;
+  }
+  __syncthreads();
+  if (sm.bad) {
+    if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+    return;
+  }
+  // a3: fill both LUTs entry-parallel: index i holds the next lut_bits stream bits (LSB-first)
+  const uint32_t LB = a.lut_bits;
+  for (uint32_t i = tid; i < 2 * lut_n; i += blockDim.x) {
+    const int t = i >= lut_n;
+    const uint32_t idx = i - (t ? lut_n : 0u);
+    const uint32_t v = __brev(idx) >> (32 - LB);      // code bits, first stream bit most significant
+    const CanonTab& T = sm.tab[t];
+    uint32_t ent = 0;                                  // 0 = unresolved (long code or invalid)
+    for (uint32_t l = 1; l <= LB; ++l) {
+      const uint32_t code = v >> (LB - l);
+      if (code - T.first[l] < T.count[l]) {
+        const uint32_t sym = t ? sm.sorted_d[T.index[l] + code - T.first[l]] : sm.sorted_ll[T.index[l] + code - T.first[l]];
+        ent = t ? d_entry(sym, l) : ll_entry(sym, l);
+        break;
+      }
+    }
+    (t ? lut_d : lut_ll)[idx] = ent;
+  }
+  __syncthreads();
+
+  // a2 + a4: sub-blocks in chunks of blockDim; CTA-wide exclusive scans give start bit and literal offset
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + kTreeBytes);
+  const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
+  const uint8_t* subt = a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total;
+  uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
+  uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
+  uint8_t* lit_base = tok + 4ull * e.n_seq;
+  const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
+  for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
+    const uint32_t k = c0 + tid;
+    uint32_t bsz = 0, nl = 0;
+    if (k < e.n_sub) {
+      const uint32_t* se = reinterpret_cast<const uint32_t*>(subt + uint64_t(kSubEntryBytes) * (e.sub_first + k));
+      bsz = __ldg(se);
+      nl = __ldg(se + 1);
+    }
+    const uint64_t ib = warp_incl_scan_u64(bsz, lane);
+    const uint32_t il = warp_incl_scan_u32(nl, lane);
+    if (lane == 31) { sm.wbits[warp] = ib; sm.wlits[warp] = il; }
+    __syncthreads();
+    uint64_t pre_b = sm.carry_bits;
+    uint32_t pre_l = sm.carry_lits;
+    for (uint32_t w = 0; w < warp; ++w) { pre_b += sm.wbits[w]; pre_l += sm.wlits[w]; }
+    uint64_t tot_b = sm.carry_bits;
+    uint32_t tot_l = sm.carry_lits;
+    for (uint32_t w = 0; w < nwarps; ++w) { tot_b += sm.wbits[w]; tot_l += sm.wlits[w]; }
+    __syncthreads();
+    if (tid == 0) { sm.carry_bits = tot_b; sm.carry_lits = tot_l; }
+    const uint64_t start = pre_b + ib - bsz;
+    const uint32_t lstart = pre_l + il - nl;
+    if (k < e.n_sub) {
+      uint32_t err = 0;
+      if (start + bsz > bit_limit || uint64_t(lstart) + nl > e.n_lit) err = 1;
+      const uint32_t seq0 = k * e.S;
+      const uint32_t nseq = (k + 1 == e.n_sub) ? e.n_seq - seq0 : e.S;
+      const bool last = k + 1 == e.n_sub;
+      uint32_t* rec = rec_base + seq0;
+      uint8_t* lit = lit_base + lstart;
+      uint32_t si = 0, lw = 0, run = 0;
+      uint64_t used = 0;
+      // bit reader: buf holds nb >= 33 valid bits after refill
+      uint64_t w = start >> 5;
+      const uint32_t sh = uint32_t(start & 31);
+      uint64_t buf = 0;
+      int nb = 0;
+      if (!err) { buf = uint64_t(__ldg(words + w)) >> sh; nb = 32 - int(sh); ++w; }
+      while (!err) {
+        if (!last && si == nseq) break;
+        if (nb <= 32) { buf |= uint64_t(__ldg(words + w)) << nb; nb += 32; ++w; }
+        uint32_t ent = lut_ll[uint32_t(buf) & lmask];
+        uint32_t len = ent & 15u;
+        if (len == 0) {                                 // code longer than the table index
+          const int sym = canon_slow(buf, sm.tab[0], sm.sorted_ll, &len);
+          if (sym < 0) { err = 2; break; }
+          ent = ll_entry(uint32_t(sym), len);
+        }
+        buf >>= len; nb -= int(len); used += len;
+        const uint32_t kind = (ent >> 4) & 3u;
+        if (kind == K_LIT) {
+          if (lw >= nl) { err = 3; break; }
+          lit[lw++] = uint8_t(ent >> 8);
+          if (++run == kMaxLitRun) {                    // R10/R16: literal-only sequence at 1023
+            if (si >= nseq) { err = 4; break; }
+            rec[si++] = kMaxLitRun;
+            run = 0;
+          }
+        } else if (kind == K_LEN) {
+          const uint32_t xb = (ent >> 17) & 7u;
+          const uint32_t L = ((ent >> 8) & 511u) + (uint32_t(buf) & ((1u << xb) - 1u));
+          buf >>= xb; nb -= int(xb); used += xb;
+          if (nb <= 32) { buf |= uint64_t(__ldg(words + w)) << nb; nb += 32; ++w; }
+          uint32_t de = lut_d[uint32_t(buf) & lmask];
+          uint32_t dl = de & 15u;
+          if (dl == 0) {
+            const int sym = canon_slow(buf, sm.tab[1], sm.sorted_d, &dl);
+            if (sym < 0) { err = 5; break; }
+            de = d_entry(uint32_t(sym), dl);
+          }
+          if (((de >> 4) & 3u) == K_BAD) { err = 5; break; }
+          buf >>= dl; nb -= int(dl); used += dl;
+          const uint32_t dx = (de >> 24) & 15u;
+          const uint32_t dist = ((de >> 8) & 0xffffu) + (uint32_t(buf) & ((1u << dx) - 1u));
+          buf >>= dx; nb -= int(dx); used += dx;
+          if (L < a.min_match || L > a.max_match || si >= nseq) { err = 6; break; }
+          rec[si++] = run | ((L - mm1) << 10) | ((dist - 1) << 16);
+          run = 0;
+        } else if (kind == K_EOB) {
+          if (!last) { err = 7; break; }
+          if (run) {
+            if (si >= nseq) { err = 4; break; }
+            rec[si++] = run;
+            run = 0;
+          }
+          break;
+        } else {
+          err = 2;
+          break;
+        }
+        if (used > bsz) { err = 8; break; }
+      }
+      if (!err && (si != nseq || run != 0 || used != bsz || lw != nl)) err = 9;
+      if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
+}
+
+// ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
+// byte copy without overlap (dist >= L, reading R2): loads are issued ahead of stores for ILP
+__device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_t n) {
+  uint32_t k = 0;
+  for (; k + 8 <= n; k += 8) {
+    uint8_t t0 = s[k], t1 = s[k + 1], t2 = s[k + 2], t3 = s[k + 3], t4 = s[k + 4], t5 = s[k + 5], t6 = s[k + 6], t7 = s[k + 7];
+    d[k] = t0; d[k + 1] = t1; d[k + 2] = t2; d[k + 3] = t3; d[k + 4] = t4; d[k + 5] = t5; d[k + 6] = t6; d[k + 7] = t7;
+  }
+  for (; k < n; ++k) d[k] = s[k];
+}
+__device__ __forceinline__ void copy_lits(uint8_t* d, const uint8_t* __restrict__ s, uint32_t n) {
+  uint32_t k = 0;
+  for (; k + 4 <= n; k += 4) {
+    uint8_t t0 = __ldg(s + k), t1 = __ldg(s + k + 1), t2 = __ldg(s + k + 2), t3 = __ldg(s + k + 3);
+    d[k] = t0; d[k + 1] = t1; d[k + 2] = t2; d[k + 3] = t3;
+  }
+  for (; k < n; ++k) d[k] = __ldg(s + k);
+}
+
+template <int STRAT, bool STATS>
+__global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int byte_mode) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wi >= a.n_blocks) return;
+  const uint32_t b = a.first_block + wi;
+  const BlockEntry e = load_entry(a.src, b, lane);
+  const uint32_t ulen = block_ulen(a, b);
+  const uint8_t* base;
+  bool ok = e.n_lit <= ulen && e.n_seq <= ulen;
+  if (byte_mode) {
+    ok = ok && payload_ok(a, e) && 4ull * e.n_seq + e.n_lit <= e.payload_len && e.S == 0 && e.n_sub == 0 && e.sub_first == 0;
+    base = a.src + e.payload_off;
+  } else {
+    ok = ok && 4ull * e.n_seq + e.n_lit <= a.max_tok;
+    base = a.tokens + uint64_t(wi) * a.tok_stride;
+  }
+  if (!ok) {
+    if (lane == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 1);
+    return;
+  }
+  const uint32_t* recs = reinterpret_cast<const uint32_t*>(base);
+  const uint8_t* lits = base + 4ull * e.n_seq;
+  uint8_t* out = a.dst + uint64_t(wi) * a.block_size;
+  const uint32_t mm1 = a.min_match - 1, n_seq = e.n_seq;
+
+  uint32_t o_carry = 0, l_carry = 0;
+  uint32_t r_next = lane < n_seq ? __ldg(recs + lane) : 0u;
+  for (uint32_t g0 = 0; g0 < n_seq; g0 += 32) {
+    const uint32_t i = g0 + lane;
+    const bool act = i < n_seq;
+    const uint32_t r = r_next;
+    r_next = (i + 32 < n_seq) ? __ldg(recs + i + 32) : 0u;  // prefetch the next group's record
+    // a5: decode the record and one packed exclusive scan (literal offset | output offset << 16)
+    const uint32_t lit = r & 1023u, mcode = (r >> 10) & 63u, dist = (r >> 16) + 1u;
+    const uint32_t L = mcode ? mcode + mm1 : 0u;
+    const uint32_t v = lit | ((lit + L) << 16);
+    const uint32_t incl = warp_incl_scan_u32(v, lane);
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    const uint32_t ex = incl - v;
+    const uint32_t lp = l_carry + (ex & 0xffffu);
+    const uint32_t op = o_carry + (ex >> 16);
+    const uint32_t dst = op + lit;
+    const uint32_t src = dst - dist;
+    // checks of FORMAT.md §2 (MalformedBackRef / CorruptStream)
+    const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst);
+    const bool bad_rec = act && !mcode && (r >> 16);
+    const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
+    const bool bad_sz = o_carry + out_sum > ulen || l_carry + lit_sum > e.n_lit;
+    if (__any_sync(FULL, bad_ref || bad_rec) || bad_sz) {
+      if (lane == 0) report(a, bad_sz || __any_sync(FULL, bad_rec) ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g0);
+      return;
+    }
+    // a6: literal strings
+    if (act) copy_lits(out + op, lits + lp, lit);
+    // a7: back-references
+    const bool has = act && L;
+    if (STRAT == GOMP_STRAT_SC) {
+      __syncwarp();
+      uint32_t m = __ballot_sync(FULL, has);
+      while (m) {
+        const uint32_t j = __ffs(m) - 1;
+        if (lane == j) copy_nolap(out + dst, out + src, L);
+        __syncwarp();
+        m &= m - 1;
+      }
+    } else {
+      bool use_mrr = STRAT == GOMP_STRAT_MRR;
+      if (STRAT == GOMP_STRAT_DE) {
+        // DE rule (FORMAT.md §4): sources below the group start or inside the lane's own literal string
+        const bool de_ok = !has || src + L <= o_carry || src >= op;
+        if (__all_sync(FULL, de_ok)) {
+          if (has) copy_nolap(out + dst, out + src, L);
+        } else {
+          use_mrr = true;
+          if (STATS && lane == 0) atomicAdd(stats_ptr(a) + 66, 1ull);
+        }
+        if (STATS && !use_mrr) {
+          const uint32_t any = __ballot_sync(FULL, has);
+          if (lane == 0) atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
+          uint32_t bytes = has ? L : 0u;
+#pragma unroll
+          for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+          if (lane == 0 && any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
+        }
+      }
+      if (use_mrr) {
+        // MRR (Fig. alg:mrr): HWM = destination of the lowest pending lane = end of the gap-free written
+        // prefix (R1); a lane is ready when its source lies below HWM or inside its own literal (R4)
+        __syncwarp();
+        bool pending = has;
+        uint32_t votes = __ballot_sync(FULL, pending);
+        uint32_t rounds = 0;
+        while (votes) {
+          const uint32_t p = __ffs(votes) - 1;
+          const uint32_t hwm = __shfl_sync(FULL, dst, p);
+          const bool ready = pending && (src + L <= hwm || src >= op);
+          if (ready) copy_nolap(out + dst, out + src, L);
+          ++rounds;
+          if (STATS) {
+            uint32_t bytes = ready ? L : 0u;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+            if (lane == 0 && rounds < 33) atomicAdd(stats_ptr(a) + 33 + rounds, (unsigned long long)bytes);
+          }
+          if (!__any_sync(FULL, ready)) {
+            if (lane == 0) report(a, GOMP_ERR_NO_PROGRESS, b, g0);
+            return;
+          }
+          pending = pending && !ready;
+          __syncwarp();
+          votes = __ballot_sync(FULL, pending);
+        }
+        if (STATS && lane == 0) atomicAdd(stats_ptr(a) + (rounds < 33 ? rounds : 32), 1ull);
+      }
+    }
+    __syncwarp();
+    o_carry += out_sum;
+    l_carry += lit_sum;
+  }
+  if (o_carry != ulen || l_carry != e.n_lit) {
+    if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+  }
+}
+
+template <int S>
+void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
+  const dim3 grid((a.n_blocks + kLz77Warps - 1) / kLz77Warps), block(32 * kLz77Warps);
+  if (stats) lz77_kernel<S, true><<<grid, block, 0, st>>>(a, byte_mode ? 1 : 0);
+  else lz77_kernel<S, false><<<grid, block, 0, st>>>(a, byte_mode ? 1 : 0);
+}
+
+size_t huff_smem_bytes(uint32_t lut_bits) {
+  return ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << lut_bits) * sizeof(uint32_t);
+}
+
+gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
+                             size_t src_len, uint8_t* d_dst, size_t dst_cap, void* d_ws, size_t ws_bytes,
+                             int strategy, cudaStream_t st) {
+  if (!info || !d_src || !d_ws || (!d_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
+  if (uint64_t(first) + nblk > info->n_blocks) return GOMP_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(d_src) | reinterpret_cast<uintptr_t>(d_ws)) & 15u) return GOMP_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(d_dst) & 15u) return GOMP_ERR_INVALID_ARG;
+  if (src_len < info->file_len) return GOMP_ERR_TRUNCATED;
+  int s = strategy & GOMP_STRAT_MASK;
+  const bool stats = (strategy & GOMP_FLAG_STATS) != 0;
+  const bool decode_only = (strategy & GOMP_FLAG_DECODE_ONLY) != 0, lz77_only = (strategy & GOMP_FLAG_LZ77_ONLY) != 0;
+  if (strategy & ~(GOMP_STRAT_MASK | GOMP_FLAG_STATS | GOMP_FLAG_DECODE_ONLY | GOMP_FLAG_LZ77_ONLY)) return GOMP_ERR_INVALID_ARG;
+  if (decode_only && lz77_only) return GOMP_ERR_INVALID_ARG;
+  if (s == GOMP_STRAT_AUTO) s = info->de ? GOMP_STRAT_DE : GOMP_STRAT_MRR;
+  if (s != GOMP_STRAT_DE && s != GOMP_STRAT_MRR && s != GOMP_STRAT_SC) return GOMP_ERR_INVALID_ARG;
+  uint64_t out_bytes = 0;
+  if (nblk) {
+    const uint64_t lo = uint64_t(first) * info->block_size;
+    const uint64_t hi = std::min<uint64_t>(uint64_t(first + nblk) * info->block_size, info->uncompressed_len);
+    out_bytes = hi - lo;
+  }
+  if (dst_cap < out_bytes) return GOMP_ERR_DST_TOO_SMALL;
+  size_t need = 0;
+  gomp_decompress_workspace_size(info, nblk ? nblk : 1, &need);
+  if (ws_bytes < need) return GOMP_ERR_WORKSPACE_TOO_SMALL;
+  if (cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  if (nblk == 0) return GOMP_OK;
+  Args a{};
+  a.src = d_src;
+  a.dst = d_dst;
+  a.ws = static_cast<uint8_t*>(d_ws);
+  a.tokens = a.ws + kWsHeaderBytes;
+  a.total = info->uncompressed_len;
+  a.file_len = info->file_len;
+  a.payload_base = info->payload_base;
+  a.tok_stride = align16(info->max_block_tokens);
+  a.first_block = first;
+  a.n_blocks = nblk;
+  a.block_size = info->block_size;
+  a.window = info->window_size;
+  a.min_match = info->min_match;
+  a.max_match = info->max_match;
+  a.cwl = info->cwl;
+  a.lut_bits = std::min<uint32_t>(info->cwl, kMaxLutBits);
+  a.max_tok = info->max_block_tokens;
+  a.n_sub_total = info->n_sub_total;
+  a.nb_total = info->n_blocks;
+  const bool byte_mode = info->mode == GOMP_MODE_BYTE;
+  if (!byte_mode && !lz77_only) {
+    // CTA size ~ sub-blocks per block (thread per sub-block), 32..256
+    const uint64_t avg = (uint64_t(info->n_sub_total) + info->n_blocks - 1) / std::max<uint32_t>(info->n_blocks, 1);
+    uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg + 31) / 32 * 32)));
+    const size_t smem = huff_smem_bytes(a.lut_bits);
+    huff_decode_kernel<<<nblk, nt, smem, st>>>(a);
+    if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
+  }
+  switch (s) {
+    case GOMP_STRAT_DE: launch_lz77<GOMP_STRAT_DE>(a, stats, byte_mode, st); break;
+    case GOMP_STRAT_MRR: launch_lz77<GOMP_STRAT_MRR>(a, stats, byte_mode, st); break;
+    default: launch_lz77<GOMP_STRAT_SC>(a, stats, byte_mode, st); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
+}
+
+}  // namespace
+}  // namespace gomp
+
+using namespace gomp;
+
+GOMP_EXPORT gomp_status gomp_decompress(const gomp_info* info, const uint8_t* d_src, size_t src_len, uint8_t* d_dst,
+                                        size_t dst_cap, void* d_ws, size_t ws_bytes, int strategy, void* stream) {
+  if (!info) return GOMP_ERR_INVALID_ARG;
+  return decompress_range(info, 0, info->n_blocks, d_src, src_len, d_dst, dst_cap, d_ws, ws_bytes, strategy,
+                          static_cast<cudaStream_t>(stream));
+}
+
+GOMP_EXPORT gomp_status gomp_decompress_blocks(const gomp_info* info, uint32_t first_block, uint32_t n_blocks,
+                                               const uint8_t* d_src, size_t src_len, uint8_t* d_dst, size_t dst_cap,
+                                               void* d_ws, size_t ws_bytes, int strategy, void* stream) {
+  return decompress_range(info, first_block, n_blocks, d_src, src_len, d_dst, dst_cap, d_ws, ws_bytes, strategy,
+                          static_cast<cudaStream_t>(stream));
+}
+
+GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_t* h_src, size_t src_len, uint8_t* h_dst,
+                                             size_t dst_cap, uint8_t* d_src_buf, uint8_t* d_dst_buf, void* d_ws,
+                                             size_t ws_bytes, int strategy, void* stream) {
+  if (!info || !h_src || !d_src_buf || (!h_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
+  if (src_len < info->file_len) return GOMP_ERR_TRUNCATED;
+  if (dst_cap < info->uncompressed_len) return GOMP_ERR_DST_TOO_SMALL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(d_src_buf, h_src, info->file_len, cudaMemcpyHostToDevice, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  gomp_status s = decompress_range(info, 0, info->n_blocks, d_src_buf, info->file_len, d_dst_buf,
+                                   info->uncompressed_len, d_ws, ws_bytes, strategy, st);
+  if (s != GOMP_OK) return s;
+  if (info->uncompressed_len &&
+      cudaMemcpyAsync(h_dst, d_dst_buf, info->uncompressed_len, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return GOMP_ERR_CUDA;
+  return GOMP_OK;
+}
+
+GOMP_EXPORT gomp_status gomp_decompress_error(const void* d_ws, void* stream, gomp_error* out) {
+  if (!d_ws || !out) return GOMP_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(out, d_ws, sizeof(gomp_error), cudaMemcpyDeviceToHost, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
+}
+
+GOMP_EXPORT gomp_status gomp_decompress_stats(const void* d_ws, void* stream, gomp_stats* out) {
+  if (!d_ws || !out) return GOMP_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(out, static_cast<const uint8_t*>(d_ws) + kWsStatsOff, sizeof(gomp_stats), cudaMemcpyDeviceToHost,
+                      st) != cudaSuccess)
+    return GOMP_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
+}

@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle, byte for byte (`-m gpu`).
+
+Inputs are seeded synthetic data of the paper's workloads. Files come from the host compressor
+(never from the CUDA path); expected bytes come from oracle.decompress() (and equal the original input).
+Sizes span several blocks and warp groups with ragged tails; the full BASELINE.json sizes are covered by
+test_full_size_* (all bytes vs the input; oracle on sampled blocks).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+import paper_1606_00519_b200 as gomp
+from fmt_util import byte_file
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _data(kind, n, seed=1):
+    if kind == "zeros":
+        return datagen.zeros(n)
+    if kind.startswith("nested"):
+        return datagen.nested(n, int(kind[6:]), seed=seed)
+    return datagen.GENERATORS[kind](n, seed=seed)
+
+
+def _gpu(c, strategy="auto", **kw):
+    return gomp.decompress(torch.as_tensor(np.asarray(c)).to(DEV), strategy=strategy, **kw)
+
+
+def _check(c, x, strategies):
+    ref = oracle.decompress(np.asarray(c))
+    assert np.array_equal(ref, x)
+    for s in strategies:
+        y = _gpu(c, s).cpu().numpy()
+        assert y.shape == ref.shape
+        if not np.array_equal(y, ref):
+            bad = np.flatnonzero(y != ref)
+            raise AssertionError(f"strategy {s}: {bad.size} bytes differ, first at {bad[0]}")
+
+
+KINDS = [("wiki", 1_100_003), ("text", 1 << 20), ("matrix", 700_001), ("nested8", 300_000), ("nested32", 200_000),
+         ("random", 150_001), ("zeros", 100_000)]
+
+
+@pytest.mark.parametrize("kind,n", KINDS)
+@pytest.mark.parametrize("de", [True, False])
+def test_byte_parity(kind, n, de):
+    x = _data(kind, n)
+    c = gomp.compress(x, mode="byte", de=de, block_size=65536)
+    _check(c, x, ["de", "mrr", "sc"] if de else ["mrr", "sc", "de"])
+
+
+@pytest.mark.parametrize("kind,n", KINDS)
+@pytest.mark.parametrize("de", [True, False])
+@pytest.mark.parametrize("sub", [("k", 16), ("S", 16)])
+def test_bit_parity(kind, n, de, sub):
+    x = _data(kind, n)
+    kw = dict(sub_blocks_per_block=sub[1], sub_block_seqs=0) if sub[0] == "k" else dict(sub_block_seqs=sub[1])
+    c = gomp.compress(x, mode="bit", de=de, block_size=65536, **kw)
+    _check(c, x, ["auto", "mrr"] if de else ["auto", "sc"])
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(block_size=16), dict(block_size=4096, window_size=1), dict(block_size=1 << 20),
+    dict(block_size=32768, min_match=3, max_match=65), dict(block_size=32768, min_match=3, max_match=3),
+    dict(block_size=32768, window_size=32768), dict(block_size=262144, sub_blocks_per_block=1, sub_block_seqs=0),
+    dict(block_size=262144, sub_block_seqs=1), dict(block_size=262144, sub_blocks_per_block=300, sub_block_seqs=0),
+])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_parameter_edges(cfg, mode):
+    x = datagen.wiki(600_000, seed=5)
+    kw = dict(cfg)
+    if mode == "bit" and "sub_block_seqs" not in kw:
+        kw["sub_block_seqs"] = 16
+    if mode == "byte":
+        kw.pop("sub_block_seqs", None)
+        kw.pop("sub_blocks_per_block", None)
+    c = gomp.compress(x, mode=mode, **kw)
+    _check(c, x, ["auto", "mrr"])
+
+
+@pytest.mark.parametrize("cwl", [9, 11, 12, 15])
+def test_code_length_limits(cwl):
+    """cwl > 11 exercises the canonical path for codes longer than the shared-memory table index."""
+    x = datagen.matrix(500_000, seed=8)
+    c = gomp.compress(x, mode="bit", cwl=cwl, block_size=131072, sub_block_seqs=0, sub_blocks_per_block=8)
+    _check(c, x, ["auto"])
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 65535, 65536, 65537, 3 * 65536 - 1])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_sizes_and_ragged_tails(n, mode):
+    x = datagen.text(n, seed=12)
+    c = gomp.compress(x, mode=mode, block_size=65536, sub_block_seqs=16)
+    ref = oracle.decompress(c.numpy())
+    y = _gpu(c).cpu().numpy()
+    assert np.array_equal(y, ref) and np.array_equal(ref, x)
+
+
+def test_hand_built_mrr_chain():
+    """Adversarial chain: lane i reads lane i-1's back-reference output (3 MRR rounds)."""
+    seqs = [(8, 8, 8), (0, 8, 8), (0, 8, 8)]
+    f = byte_file([(seqs, b"ABCDEFGH")], block_size=64)
+    for s in ("mrr", "sc", "de"):
+        y, st = _gpu(f, s, return_stats=True)
+        assert bytes(y.cpu().numpy()) == b"ABCDEFGH" * 4
+    y, st = _gpu(f, "mrr", return_stats=True)
+    assert st["rounds"][3] == 1 and st["bytes"][1:4] == [8, 8, 8]
+    _, st = _gpu(f, "de", return_stats=True)
+    assert st["de_fallback_groups"] == 1
+
+
+@pytest.mark.parametrize("kind", ["wiki", "matrix", "nested4", "nested16", "nested32"])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_mrr_statistics_match_oracle_model(kind, mode):
+    x = _data(kind, 400_000, seed=3)
+    c = gomp.compress(x, mode=mode, de=False, block_size=65536, sub_block_seqs=16)
+    hist, nbytes = oracle.mrr_simulate(c.numpy())
+    y, st = _gpu(c, "mrr", return_stats=True)
+    assert np.array_equal(y.cpu().numpy(), x)
+    assert st["rounds"] == [int(v) for v in hist]
+    assert st["bytes"][1:] == [int(v) for v in nbytes[1:]]
+    cd = gomp.compress(x, mode=mode, de=True, block_size=65536, sub_block_seqs=16)
+    hd, bd = oracle.mrr_simulate(cd.numpy())
+    for s in ("de", "mrr"):
+        y, st = _gpu(cd, s, return_stats=True)
+        assert np.array_equal(y.cpu().numpy(), x)
+        assert st["rounds"] == [int(v) for v in hd] and st["de_fallback_groups"] == 0
+
+
+def _expect(status, f, strategy="auto"):
+    with pytest.raises(gomp.GompError) as e:
+        _gpu(f, strategy)
+    assert e.value.name == status, e.value
+
+
+def test_device_errors_byte():
+    _expect("MALFORMED_BACKREF", byte_file([([(4, 4, 2)], b"abcd")], block_size=16))          # overlap (R2)
+    _expect("MALFORMED_BACKREF", byte_file([([(2, 4, 5)], b"ab")], block_size=16))            # before block
+    _expect("MALFORMED_BACKREF", byte_file([([(16, 0, 0)], b"a" * 16), ([(8, 4, 8), (0, 4, 12)], b"b" * 8)],
+                                           block_size=16, window=8))                          # beyond window
+    f = byte_file([([(3, 0, 0)], b"abc")], block_size=16)
+    f[24] = 4
+    _expect("CORRUPT_STREAM", f)
+    x = datagen.text(100_000)
+    c = gomp.compress(x, mode="byte", block_size=16384).numpy().copy()
+    c[64 + 32 * 2 + 12] += 1     # n_seq of block 2: payload no longer adds up
+    with pytest.raises(gomp.GompError) as e:
+        _gpu(c)
+    assert e.value.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT") and e.value.block == 2
+
+
+def test_device_errors_bit_fuzz():
+    """Bit flips in payloads are detected (or decode to wrong bytes) without crashing; tables are checked."""
+    import struct
+    x = datagen.wiki(200_000, seed=2)
+    c = gomp.compress(x, mode="bit", block_size=32768, sub_block_seqs=0, sub_blocks_per_block=8).numpy()
+    off = struct.unpack_from("<Q", c.tobytes(), 64)[0]
+    rng = np.random.default_rng(0)
+    for _ in range(30):
+        bad = c.copy()
+        pos = int(rng.integers(off, off + 3000))
+        bad[pos] ^= np.uint8(1 << int(rng.integers(0, 8)))
+        try:
+            y = _gpu(bad).cpu().numpy()
+            assert not np.array_equal(y, x) or pos < off + 160
+        except gomp.GompError as e:
+            assert e.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF"), e
+    bad = c.copy()
+    bad[64 + 12] += 1  # n_seq of block 0
+    with pytest.raises(gomp.GompError) as e:
+        _gpu(bad)
+    assert e.value.name == "HEADER_INCONSISTENT" and e.value.block == 0
+
+
+def test_blocks_range_and_shards():
+    """gomp_decompress_blocks on shard ranges == the matching slice of the whole output."""
+    x = datagen.wiki(3_000_000, seed=6)
+    c = gomp.compress(x, mode="bit", block_size=131072)
+    info = gomp.get_info(c)
+    d = c.to(DEV)
+    for n_dev in (2, 3, 8):
+        first = gomp.plan_shards(c, n_dev)
+        parts = []
+        for k in range(n_dev):
+            b0, b1 = first[k], first[k + 1]
+            lo, hi = b0 * info.block_size, min(b1 * info.block_size, info.uncompressed_len)
+            out = torch.empty(max(hi - lo, 1), dtype=torch.uint8, device=DEV)
+            ws = torch.empty(gomp.workspace_size(info, max(b1 - b0, 1)), dtype=torch.uint8, device=DEV)
+            gomp.decompress_into(info, d, out, ws, first_block=b0, n_blocks=b1 - b0)
+            e = gomp.read_error(ws)
+            assert e.status == 0
+            parts.append(out[: hi - lo].cpu().numpy())
+        assert np.array_equal(np.concatenate(parts), x)
+
+
+def test_host_end_to_end():
+    x = datagen.wiki(2_000_000, seed=7)
+    for mode in ("byte", "bit"):
+        c = gomp.compress(x, mode=mode).pin_memory()
+        y = gomp.decompress_host(c, device=DEV)
+        assert np.array_equal(y.numpy(), x)
+
+
+def test_bad_arguments():
+    x = datagen.text(10_000)
+    c = gomp.compress(x, mode="byte", block_size=4096)
+    info = gomp.get_info(c)
+    d = c.to(DEV)
+    out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device=DEV)
+    ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device=DEV)
+    with pytest.raises(gomp.GompError) as e:
+        gomp.decompress_into(info, d, out[: info.uncompressed_len - 1], ws)
+    assert e.value.name == "DST_TOO_SMALL"
+    with pytest.raises(gomp.GompError) as e:
+        gomp.decompress_into(info, d[: info.file_len - 1], out, ws)
+    assert e.value.name == "TRUNCATED"
+    with pytest.raises(gomp.GompError) as e:
+        gomp.decompress_into(info, d, out, ws, strategy=9)
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(gomp.GompError) as e:
+        gomp.decompress_into(info, d, out[1:], ws)
+    assert e.value.name == "INVALID_ARG"  # misaligned output
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3-byte-mrr", "C3-bit-de"])
+def test_full_size_configs(cfg):
+    """BASELINE.json configs at full size, in the launch configuration bench.py times: every output byte vs
+    the original input, and the oracle on sampled blocks."""
+    if cfg == "C1":
+        x = datagen.text(1 << 20, seed=1)
+        c = gomp.compress(x, mode="byte", de=True, block_size=65536)
+    elif cfg == "C2":
+        x = datagen.wiki(256 << 20, seed=2)
+        c = gomp.compress(x, mode="bit", de=True, block_size=262144, sub_blocks_per_block=16)
+    elif cfg == "C3-byte-mrr":
+        x = datagen.nested(256 << 20, 8, seed=3)
+        c = gomp.compress(x, mode="byte", de=False, block_size=262144)
+    else:
+        x = datagen.nested(256 << 20, 8, seed=3)
+        c = gomp.compress(x, mode="bit", de=True, block_size=262144, sub_block_seqs=16)
+    info = gomp.get_info(c)
+    y = _gpu(c).cpu().numpy()
+    assert np.array_equal(y, x)
+    rng = np.random.default_rng(0)
+    cn = c.numpy()
+    bs = info.block_size
+    for b in sorted(set([0, info.n_blocks - 1] + [int(v) for v in rng.integers(0, info.n_blocks, 6)])):
+        ref = oracle.decompress_blocks(cn, b, b + 1, bs)
+        assert np.array_equal(y[b * bs: b * bs + len(ref)], ref)

@@ -1,0 +1,132 @@
+"""Host-side tests of libgompresso.so (CPU only): the C ABI loads and exports every symbol include/gomp.h
+declares; the host compressor writes files the oracle decodes (and, with the exhaustive match finder, the very
+same bytes as the oracle's compressor); header/table validation; the multi-GPU shard planner."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+import paper_1606_00519_b200 as gomp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gomp.h")).read()
+    return sorted(set(re.findall(r"\b(gomp_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", gomp.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (gomp_\w+)", out))
+    declared = _declared()
+    assert declared and set(declared) <= exported, set(declared) - exported
+    assert set(declared) == set(gomp.EXPORTS)
+    gomp.lib()  # loads
+    assert gomp.lib().gomp_version() == 1
+
+
+def test_library_not_named_libgomp():
+    assert os.path.basename(gomp.LIB_PATH) == "libgompresso.so"
+
+
+def test_status_strings():
+    for code, name in gomp.STATUS.items():
+        assert gomp.lib().gomp_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("kind,n", [("wiki", 120_000), ("matrix", 90_000), ("random", 30_000), ("zeros", 40_000),
+                                    ("nested4", 50_000), ("text", 0), ("text", 1), ("text", 17)])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+@pytest.mark.parametrize("de", [True, False])
+def test_compressor_matches_oracle_bytes(kind, n, mode, de):
+    if kind == "zeros":
+        x = datagen.zeros(n)
+    elif kind.startswith("nested"):
+        x = datagen.nested(n, int(kind[6:]))
+    else:
+        x = datagen.GENERATORS[kind](n, seed=4)
+    kw = dict(mode=mode, de=de, block_size=32768)
+    if mode == "bit":
+        kw.update(sub_block_seqs=0, sub_blocks_per_block=16)
+    c = gomp.compress(x, **kw).numpy()
+    ref = oracle.compress(x, **kw)
+    assert np.array_equal(c, ref)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_compressor_deterministic_across_threads(threads):
+    x = datagen.wiki(400_000, seed=9)
+    a = gomp.compress(x, mode="bit", block_size=65536, n_threads=threads).numpy()
+    b = gomp.compress(x, mode="bit", block_size=65536, n_threads=1).numpy()
+    assert np.array_equal(a, b)
+    assert np.array_equal(oracle.decompress(a), x)
+
+
+@pytest.mark.parametrize("finder,chain", [(1, 0), (0, 4)])
+def test_fast_match_finders_round_trip(finder, chain):
+    x = datagen.wiki(300_000, seed=2)
+    for mode in ("byte", "bit"):
+        c = gomp.compress(x, mode=mode, de=True, block_size=65536, match_finder=finder, max_chain=chain).numpy()
+        assert np.array_equal(oracle.decompress(c), x)
+        assert oracle.verify_de(c)
+
+
+def test_params_defaults_are_the_papers():
+    p = gomp.params()
+    assert (p.block_size, p.window_size, p.max_match, p.sub_block_seqs, p.cwl, p.min_staleness) == \
+        (262144, 8192, 64, 16, 10, 1024)
+
+
+def test_get_info_and_validation():
+    x = datagen.text(50_000)
+    c = gomp.compress(x, mode="bit", block_size=16384, sub_blocks_per_block=4)
+    info = gomp.get_info(c)
+    assert info.uncompressed_len == 50_000 and info.n_blocks == 4 and info.mode == 1 and info.de == 1
+    assert info.file_len == c.numel() and info.n_sub_total == 16
+    gomp.validate_tables(c)
+    bad = c.clone()
+    bad[0] = 0
+    with pytest.raises(gomp.GompError) as e:
+        gomp.get_info(bad)
+    assert e.value.name == "BAD_MAGIC"
+    bad = c.clone()
+    bad[4] = 9
+    with pytest.raises(gomp.GompError) as e:
+        gomp.get_info(bad)
+    assert e.value.name == "UNSUPPORTED_VERSION"
+    with pytest.raises(gomp.GompError) as e:
+        gomp.get_info(c[:63])
+    assert e.value.name == "TRUNCATED"
+    bad = c.clone()
+    bad[64 + 32 + 12] += 1  # n_seq of block 1 -> n_sub mismatch
+    with pytest.raises(gomp.GompError) as e:
+        gomp.validate_tables(bad)
+    assert e.value.name == "HEADER_INCONSISTENT" and e.value.block == 1
+
+
+def test_workspace_size():
+    x = datagen.text(70_000)
+    cb = gomp.compress(x, mode="byte", block_size=16384)
+    assert gomp.workspace_size(gomp.get_info(cb)) == 1024
+    ct = gomp.compress(x, mode="bit", block_size=16384)
+    info = gomp.get_info(ct)
+    assert gomp.workspace_size(info) >= 1024 + info.n_blocks * info.max_block_tokens
+
+
+@pytest.mark.parametrize("n_dev", [1, 2, 3, 4, 8])
+def test_plan_shards_balanced(n_dev):
+    import struct
+    x = datagen.wiki(2_000_000, seed=3)
+    c = gomp.compress(x, mode="bit", block_size=65536).numpy()
+    first = gomp.plan_shards(c, n_dev)
+    nb = gomp.get_info(c).n_blocks
+    assert first[0] == 0 and first[-1] == nb and all(a <= b for a, b in zip(first, first[1:]))
+    sizes = [sum(struct.unpack_from("<I", c.tobytes(), 64 + 32 * b + 8)[0] for b in range(first[d], first[d + 1]))
+             for d in range(n_dev)]
+    avg_block = sum(sizes) / nb
+    assert max(sizes) - min(sizes) <= 2 * avg_block + 1
