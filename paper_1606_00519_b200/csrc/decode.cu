@@ -25,7 +25,7 @@ namespace gomp {
 namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
-constexpr int kLz77Warps = 4;        // warps (= data blocks) per CTA of the LZ77 kernel
+constexpr int kLz77Warps = 2;        // warps (= data blocks) per CTA of the LZ77 kernel
 constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
 
 // workspace layout (kWsHeaderBytes = 1024): [0,16) gomp_error; [64, 64+8*67) gomp_stats; token buffer at 1024
@@ -38,7 +38,7 @@ struct Args {
   uint8_t* ws;            // workspace base (error word, stats)
   uint64_t total, file_len, payload_base, tok_stride;
   uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, lut_bits, max_tok;
-  uint32_t n_sub_total, nb_total;
+  uint32_t n_sub_total, nb_total, ring_bytes;
 };
 
 // ------------------------------------------------------------------ completion: error word (a9)
@@ -160,6 +160,38 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
+// LSB-first bit reader over a 16-byte aligned word stream with three 16-byte chunks prefetched in registers
+// (~256 bits, i.e. ~30 symbols, ahead of the decoder) so the global-load latency stays off the per-symbol
+// dependency chain. Loads are clamped to the last 16 bytes of the file (in bounds, values unused).
+struct BitIn {
+  const uint4* p;
+  const uint4* pmax;
+  uint4 q0, q1, q2;
+  uint32_t qi;
+  uint64_t buf;
+  int nb;
+  __device__ __forceinline__ uint4 ld(const uint4* c) const { return __ldg(c <= pmax ? c : pmax); }
+  __device__ __forceinline__ uint32_t word() const { return qi == 0 ? q0.x : qi == 1 ? q0.y : qi == 2 ? q0.z : q0.w; }
+  __device__ __forceinline__ void advance() {
+    if (++qi == 4) { qi = 0; q0 = q1; q1 = q2; q2 = ld(p); ++p; }
+  }
+  __device__ __forceinline__ void init(const uint32_t* words, uint64_t start, const uint4* pm) {
+    pmax = pm;
+    const uint64_t w = start >> 5;
+    const uint4* c = reinterpret_cast<const uint4*>(words) + (w >> 2);
+    q0 = ld(c); q1 = ld(c + 1); q2 = ld(c + 2);
+    p = c + 3;
+    qi = uint32_t(w & 3);
+    const uint32_t sh = uint32_t(start & 31);
+    buf = uint64_t(word()) >> sh;
+    nb = 32 - int(sh);
+    advance();
+  }
+  __device__ __forceinline__ void refill() {   // afterwards nb >= 33
+    if (nb <= 32) { buf |= uint64_t(word()) << nb; nb += 32; advance(); }
+  }
+};
+
 // ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
 __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -272,6 +304,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
+  const uint4* pmax = reinterpret_cast<const uint4*>(a.src + a.file_len - 16);
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
     uint32_t bsz = 0, nl = 0;
@@ -304,15 +337,13 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       uint8_t* lit = lit_base + lstart;
       uint32_t si = 0, lw = 0, run = 0;
       uint64_t used = 0;
-      // bit reader: buf holds nb >= 33 valid bits after refill
-      uint64_t w = start >> 5;
-      const uint32_t sh = uint32_t(start & 31);
-      uint64_t buf = 0;
-      int nb = 0;
-      if (!err) { buf = uint64_t(__ldg(words + w)) >> sh; nb = 32 - int(sh); ++w; }
+      BitIn in;
+      if (!err) in.init(words, start, pmax);
+      uint64_t& buf = in.buf;
+      int& nb = in.nb;
       while (!err) {
         if (!last && si == nseq) break;
-        if (nb <= 32) { buf |= uint64_t(__ldg(words + w)) << nb; nb += 32; ++w; }
+        in.refill();
         uint32_t ent = lut_ll[uint32_t(buf) & lmask];
         uint32_t len = ent & 15u;
         if (len == 0) {                                 // code longer than the table index
@@ -334,7 +365,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
           const uint32_t xb = (ent >> 17) & 7u;
           const uint32_t L = ((ent >> 8) & 511u) + (uint32_t(buf) & ((1u << xb) - 1u));
           buf >>= xb; nb -= int(xb); used += xb;
-          if (nb <= 32) { buf |= uint64_t(__ldg(words + w)) << nb; nb += 32; ++w; }
+          in.refill();
           uint32_t de = lut_d[uint32_t(buf) & lmask];
           uint32_t dl = de & 15u;
           if (dl == 0) {
@@ -373,7 +404,17 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
 }
 
 // ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
-// byte copy without overlap (dist >= L, reading R2): loads are issued ahead of stores for ILP
+//
+// Output goes through a per-warp shared-memory ring holding the last RING bytes of the block (RING >= window
+// + group output), so back-reference sources are read on chip; completed 16-byte chunks are flushed to HBM
+// with coalesced 16-byte stores. Literal bytes are staged into a per-warp shared-memory ring ahead of use
+// with cp.async (LDGSTS) in 512-byte units; records are prefetched four groups ahead in registers. A group too
+// large for the rings (e.g. 32 literal runs of 1023 bytes) is processed directly in global memory.
+constexpr uint32_t kLitRing = 2048;
+constexpr uint32_t kLitUnit = 512;   // 32 lanes x 16 B per cp.async instruction
+constexpr uint32_t kLitAhead = 1024; // prefetch distance in literal bytes
+
+// byte-granular copy without overlap (dist >= L, reading R2), global memory (slow path)
 __device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_t n) {
   uint32_t k = 0;
   for (; k + 8 <= n; k += 8) {
@@ -382,7 +423,7 @@ __device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_
   }
   for (; k < n; ++k) d[k] = s[k];
 }
-__device__ __forceinline__ void copy_lits(uint8_t* d, const uint8_t* __restrict__ s, uint32_t n) {
+__device__ __forceinline__ void copy_lits_global(uint8_t* d, const uint8_t* __restrict__ s, uint32_t n) {
   uint32_t k = 0;
   for (; k + 4 <= n; k += 4) {
     uint8_t t0 = __ldg(s + k), t1 = __ldg(s + k + 1), t2 = __ldg(s + k + 2), t3 = __ldg(s + k + 3);
@@ -391,11 +432,131 @@ __device__ __forceinline__ void copy_lits(uint8_t* d, const uint8_t* __restrict_
   for (; k < n; ++k) d[k] = __ldg(s + k);
 }
 
+// Copy n bytes between power-of-two shared-memory rings (masks dm/sm = size-1), source range not overlapping
+// the destination range: byte head until the destination is word aligned, then aligned 32-bit stores of
+// funnel-shifted source words (bytes of a source word outside [s, s+n) are discarded), byte tail.
+__device__ __forceinline__ void ring_copy(uint8_t* D, uint32_t dm, uint32_t d, const uint8_t* S, uint32_t sm,
+                                          uint32_t s, uint32_t n) {
+  uint32_t h = (4u - (d & 3u)) & 3u;
+  if (h > n) h = n;
+  for (uint32_t k = 0; k < h; ++k) D[(d + k) & dm] = S[(s + k) & sm];
+  d += h; s += h; n -= h;
+  const uint32_t nw = n >> 2;
+  if (nw) {
+    const uint32_t* S32 = reinterpret_cast<const uint32_t*>(S);
+    uint32_t* D32 = reinterpret_cast<uint32_t*>(D);
+    const uint32_t swm = sm >> 2, dwm = dm >> 2, sh = (s & 3u) * 8u;
+    uint32_t sw = s >> 2, dw = d >> 2;
+    uint32_t lo = S32[sw & swm];
+    for (uint32_t k = 0; k < nw; ++k) {
+      const uint32_t hi = S32[(sw + 1) & swm];
+      D32[dw & dwm] = __funnelshift_r(lo, hi, sh);
+      lo = hi; ++sw; ++dw;
+    }
+    d += nw * 4; s += nw * 4; n -= nw * 4;
+  }
+  for (uint32_t k = 0; k < n; ++k) D[(d + k) & dm] = S[(s + k) & sm];
+}
+
+struct GlobalOut {
+  uint8_t* out;
+  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { copy_nolap(out + dst, out + src, n); }
+};
+struct RingOut {
+  uint8_t* ring;
+  uint32_t rm;
+  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy(ring, rm, dst, ring, rm, src, n); }
+};
+
+// a7 for one warp group: back-references of the lanes with has = (L > 0). Returns false on NO_PROGRESS.
+template <int STRAT, bool STATS, class Out>
+__device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint32_t lane, bool has, uint32_t dst,
+                                              uint32_t src, uint32_t L, uint32_t op, uint32_t o_carry, uint32_t b,
+                                              uint32_t g0) {
+  if (STRAT == GOMP_STRAT_SC) {          // Sequential Copying
+    __syncwarp();
+    uint32_t m = __ballot_sync(FULL, has);
+    while (m) {
+      const uint32_t j = __ffs(m) - 1;
+      if (lane == j) o.copy(dst, src, L);
+      __syncwarp();
+      m &= m - 1;
+    }
+    return true;
+  }
+  bool use_mrr = STRAT == GOMP_STRAT_MRR;
+  if (STRAT == GOMP_STRAT_DE) {
+    // DE rule (FORMAT.md §4): every source lies below the group start or inside the lane's own literal, so
+    // all lanes copy in one round with no inter-lane ordering
+    const bool de_ok = !has || src + L <= o_carry || src >= op;
+    if (__all_sync(FULL, de_ok)) {
+      if (has) o.copy(dst, src, L);
+      if (STATS) {
+        const uint32_t any = __ballot_sync(FULL, has);
+        uint32_t bytes = has ? L : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+        if (lane == 0) {
+          atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
+          if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
+        }
+      }
+    } else {
+      use_mrr = true;
+      if (STATS && lane == 0) atomicAdd(stats_ptr(a) + 66, 1ull);
+    }
+  }
+  if (use_mrr) {
+    // MRR (Fig. alg:mrr): HWM = destination of the lowest pending lane = end of the gap-free written prefix
+    // (R1); a lane is ready when its source lies below HWM or inside its own literal string (R4)
+    __syncwarp();
+    bool pending = has;
+    uint32_t votes = __ballot_sync(FULL, pending);
+    uint32_t rounds = 0;
+    while (votes) {
+      const uint32_t p = __ffs(votes) - 1;
+      const uint32_t hwm = __shfl_sync(FULL, dst, p);
+      const bool ready = pending && (src + L <= hwm || src >= op);
+      if (ready) o.copy(dst, src, L);
+      ++rounds;
+      if (STATS) {
+        uint32_t bytes = ready ? L : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+        if (lane == 0 && rounds < 33) atomicAdd(stats_ptr(a) + 33 + rounds, (unsigned long long)bytes);
+      }
+      if (!__any_sync(FULL, ready)) {
+        if (lane == 0) report(a, GOMP_ERR_NO_PROGRESS, b, g0);
+        return false;
+      }
+      pending = pending && !ready;
+      __syncwarp();
+      votes = __ballot_sync(FULL, pending);
+    }
+    if (STATS && lane == 0) atomicAdd(stats_ptr(a) + (rounds < 33 ? rounds : 32), 1ull);
+  }
+  return true;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait(uint32_t allowed) {
+  if (allowed >= 2) asm volatile("cp.async.wait_group 2;\n" ::);
+  else if (allowed == 1) asm volatile("cp.async.wait_group 1;\n" ::);
+  else asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 template <int STRAT, bool STATS>
 __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int byte_mode) {
+  extern __shared__ __align__(16) uint8_t lz_smem[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wi >= a.n_blocks) return;
+  const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLitRing - 1;
+  uint8_t* ring = lz_smem + (threadIdx.x >> 5) * (RING + kLitRing);
+  uint8_t* lring = ring + RING;
   const uint32_t b = a.first_block + wi;
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
@@ -414,16 +575,28 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   }
   const uint32_t* recs = reinterpret_cast<const uint32_t*>(base);
   const uint8_t* lits = base + 4ull * e.n_seq;
+  // literal stream staging: rel position = byte offset from the 16-aligned address below the stream
+  const uint8_t* lal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits) & ~uintptr_t(15));
+  const uint32_t lofs = uint32_t(lits - lal);
+  const uint32_t lend16 = (lofs + e.n_lit + 15u) & ~15u;
+  const uint32_t lring_s = uint32_t(__cvta_generic_to_shared(lring));
+  uint32_t lf = 0;  // literal bytes (rel) issued to the ring, multiple of kLitUnit
   uint8_t* out = a.dst + uint64_t(wi) * a.block_size;
   const uint32_t mm1 = a.min_match - 1, n_seq = e.n_seq;
+  const RingOut ro{ring, RM};
+  const GlobalOut go{out};
 
-  uint32_t o_carry = 0, l_carry = 0;
-  uint32_t r_next = lane < n_seq ? __ldg(recs + lane) : 0u;
+  uint32_t o_carry = 0, l_carry = 0, flushed = 0;
+  uint32_t rq0 = lane < n_seq ? __ldg(recs + lane) : 0u;
+  uint32_t rq1 = lane + 32 < n_seq ? __ldg(recs + lane + 32) : 0u;
+  uint32_t rq2 = lane + 64 < n_seq ? __ldg(recs + lane + 64) : 0u;
+  uint32_t rq3 = lane + 96 < n_seq ? __ldg(recs + lane + 96) : 0u;
   for (uint32_t g0 = 0; g0 < n_seq; g0 += 32) {
     const uint32_t i = g0 + lane;
     const bool act = i < n_seq;
-    const uint32_t r = r_next;
-    r_next = (i + 32 < n_seq) ? __ldg(recs + i + 32) : 0u;  // prefetch the next group's record
+    const uint32_t r = rq0;
+    rq0 = rq1; rq1 = rq2; rq2 = rq3;
+    rq3 = (i + 128 < n_seq) ? __ldg(recs + i + 128) : 0u;
     // a5: decode the record and one packed exclusive scan (literal offset | output offset << 16)
     const uint32_t lit = r & 1023u, mcode = (r >> 10) & 63u, dist = (r >> 16) + 1u;
     const uint32_t L = mcode ? mcode + mm1 : 0u;
@@ -435,7 +608,6 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
     const uint32_t op = o_carry + (ex >> 16);
     const uint32_t dst = op + lit;
     const uint32_t src = dst - dist;
-    // checks of FORMAT.md §2 (MalformedBackRef / CorruptStream)
     const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst);
     const bool bad_rec = act && !mcode && (r >> 16);
     const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
@@ -444,83 +616,75 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       if (lane == 0) report(a, bad_sz || __any_sync(FULL, bad_rec) ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g0);
       return;
     }
-    // a6: literal strings
-    if (act) copy_lits(out + op, lits + lp, lit);
-    // a7: back-references
     const bool has = act && L;
-    if (STRAT == GOMP_STRAT_SC) {
+    const bool fast = out_sum + a.window + 16 <= RING && lit_sum + kLitAhead <= kLitRing;
+    if (fast) {
+      // stage the group's literals (rel range [lofs + l_carry, need)) into the literal ring
+      const uint32_t need = lofs + l_carry + lit_sum;
+      while (lf < need + kLitAhead && lf < lend16 && lf + kLitUnit <= lofs + l_carry + kLitRing) {
+        const uint32_t off = lf + lane * 16;
+        if (off < lend16) cp_async16(lring_s + (off & LM), lal + off);
+        cp_commit();
+        lf += kLitUnit;
+      }
+      const uint32_t issued = lf / kLitUnit, needed = (need + kLitUnit - 1) / kLitUnit;
+      cp_wait(issued > needed ? issued - needed : 0u);
       __syncwarp();
-      uint32_t m = __ballot_sync(FULL, has);
-      while (m) {
-        const uint32_t j = __ffs(m) - 1;
-        if (lane == j) copy_nolap(out + dst, out + src, L);
-        __syncwarp();
-        m &= m - 1;
-      }
+      // a6: literal strings into the output ring
+      if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+      // a7: back-references inside the ring
+      if (!resolve_group<STRAT, STATS>(a, ro, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+      __syncwarp();
+      // flush completed 16-byte chunks to HBM (coalesced 16-byte stores)
+      const uint32_t q1 = (o_carry + out_sum) >> 4;
+      for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
+        reinterpret_cast<uint4*>(out)[q] = reinterpret_cast<const uint4*>(ring)[q & (RM >> 4)];
+      if (q1 * 16 > flushed) flushed = q1 * 16;
     } else {
-      bool use_mrr = STRAT == GOMP_STRAT_MRR;
-      if (STRAT == GOMP_STRAT_DE) {
-        // DE rule (FORMAT.md §4): sources below the group start or inside the lane's own literal string
-        const bool de_ok = !has || src + L <= o_carry || src >= op;
-        if (__all_sync(FULL, de_ok)) {
-          if (has) copy_nolap(out + dst, out + src, L);
-        } else {
-          use_mrr = true;
-          if (STATS && lane == 0) atomicAdd(stats_ptr(a) + 66, 1ull);
-        }
-        if (STATS && !use_mrr) {
-          const uint32_t any = __ballot_sync(FULL, has);
-          if (lane == 0) atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
-          uint32_t bytes = has ? L : 0u;
-#pragma unroll
-          for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
-          if (lane == 0 && any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
-        }
-      }
-      if (use_mrr) {
-        // MRR (Fig. alg:mrr): HWM = destination of the lowest pending lane = end of the gap-free written
-        // prefix (R1); a lane is ready when its source lies below HWM or inside its own literal (R4)
-        __syncwarp();
-        bool pending = has;
-        uint32_t votes = __ballot_sync(FULL, pending);
-        uint32_t rounds = 0;
-        while (votes) {
-          const uint32_t p = __ffs(votes) - 1;
-          const uint32_t hwm = __shfl_sync(FULL, dst, p);
-          const bool ready = pending && (src + L <= hwm || src >= op);
-          if (ready) copy_nolap(out + dst, out + src, L);
-          ++rounds;
-          if (STATS) {
-            uint32_t bytes = ready ? L : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
-            if (lane == 0 && rounds < 33) atomicAdd(stats_ptr(a) + 33 + rounds, (unsigned long long)bytes);
-          }
-          if (!__any_sync(FULL, ready)) {
-            if (lane == 0) report(a, GOMP_ERR_NO_PROGRESS, b, g0);
-            return;
-          }
-          pending = pending && !ready;
-          __syncwarp();
-          votes = __ballot_sync(FULL, pending);
-        }
-        if (STATS && lane == 0) atomicAdd(stats_ptr(a) + (rounds < 33 ? rounds : 32), 1ull);
-      }
+      // group too large for the rings: flush the ring, run the group in global memory, reload the window
+      __syncwarp();
+      for (uint32_t p = flushed + lane; p < o_carry; p += 32) out[p] = ring[p & RM];
+      flushed = o_carry;
+      __syncwarp();
+      if (act) copy_lits_global(out + op, lits + lp, lit);
+      if (!resolve_group<STRAT, STATS>(a, go, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+      __syncwarp();
+      const uint32_t o_new = o_carry + out_sum;
+      const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
+      for (uint32_t p = o_new - keep + lane; p < o_new; p += 32) ring[p & RM] = out[p];
+      flushed = o_new;
+      cp_wait(0);
+      lf = ((lofs + l_carry + lit_sum) / kLitUnit) * kLitUnit;
+      __syncwarp();
     }
-    __syncwarp();
     o_carry += out_sum;
     l_carry += lit_sum;
   }
+  cp_wait(0);
+  __syncwarp();
   if (o_carry != ulen || l_carry != e.n_lit) {
     if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+    return;
   }
+  const uint32_t q1 = o_carry >> 4;
+  for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
+    reinterpret_cast<uint4*>(out)[q] = reinterpret_cast<const uint4*>(ring)[q & (RM >> 4)];
+  for (uint32_t p = max(q1 * 16, flushed) + lane; p < o_carry; p += 32) out[p] = ring[p & RM];
 }
+
+size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * (ring + kLitRing); }
 
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
   const dim3 grid((a.n_blocks + kLz77Warps - 1) / kLz77Warps), block(32 * kLz77Warps);
-  if (stats) lz77_kernel<S, true><<<grid, block, 0, st>>>(a, byte_mode ? 1 : 0);
-  else lz77_kernel<S, false><<<grid, block, 0, st>>>(a, byte_mode ? 1 : 0);
+  const size_t smem = lz77_smem_bytes(a.ring_bytes);
+  if (stats) {
+    cudaFuncSetAttribute(lz77_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    lz77_kernel<S, true><<<grid, block, smem, st>>>(a, byte_mode ? 1 : 0);
+  } else {
+    cudaFuncSetAttribute(lz77_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    lz77_kernel<S, false><<<grid, block, smem, st>>>(a, byte_mode ? 1 : 0);
+  }
 }
 
 size_t huff_smem_bytes(uint32_t lut_bits) {
@@ -574,6 +738,8 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   a.max_tok = info->max_block_tokens;
   a.n_sub_total = info->n_sub_total;
   a.nb_total = info->n_blocks;
+  a.ring_bytes = 16384;
+  while (a.ring_bytes < info->window_size + 4096) a.ring_bytes <<= 1;
   const bool byte_mode = info->mode == GOMP_MODE_BYTE;
   if (!byte_mode && !lz77_only) {
     // CTA size ~ sub-blocks per block (thread per sub-block), 32..256

@@ -173,6 +173,11 @@ def test_device_errors_bit_fuzz():
     bad[64 + 12] += 1  # n_seq of block 0
     with pytest.raises(gomp.GompError) as e:
         _gpu(bad)
+    assert e.value.name in ("HEADER_INCONSISTENT", "CORRUPT_STREAM") and e.value.block == 0
+    bad = c.copy()
+    bad[64 + 24] += 1  # S of block 0: n_sub no longer ceil(n_seq / S)
+    with pytest.raises(gomp.GompError) as e:
+        _gpu(bad)
     assert e.value.name == "HEADER_INCONSISTENT" and e.value.block == 0
 
 
