@@ -160,35 +160,33 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
-// LSB-first bit reader over a 16-byte aligned word stream with three 16-byte chunks prefetched in registers
-// (~256 bits, i.e. ~30 symbols, ahead of the decoder) so the global-load latency stays off the per-symbol
-// dependency chain. Loads are clamped to the last 16 bytes of the file (in bounds, values unused).
+// LSB-first bit reader: 64-bit buffer + the next 32-bit word already loaded, refilled branch-free (predicated)
+// so lanes decoding different sub-blocks stay converged. Sequential words of one thread hit L1 after the first
+// touch of each 128-byte line. Word indices are clamped to the file (values past the stream are never used).
 struct BitIn {
-  const uint4* p;
-  const uint4* pmax;
-  uint4 q0, q1, q2;
-  uint32_t qi;
+  const uint32_t* words;
+  uint32_t wlim;
+  uint32_t w, nextw;
   uint64_t buf;
   int nb;
-  __device__ __forceinline__ uint4 ld(const uint4* c) const { return __ldg(c <= pmax ? c : pmax); }
-  __device__ __forceinline__ uint32_t word() const { return qi == 0 ? q0.x : qi == 1 ? q0.y : qi == 2 ? q0.z : q0.w; }
-  __device__ __forceinline__ void advance() {
-    if (++qi == 4) { qi = 0; q0 = q1; q1 = q2; q2 = ld(p); ++p; }
-  }
-  __device__ __forceinline__ void init(const uint32_t* words, uint64_t start, const uint4* pm) {
-    pmax = pm;
-    const uint64_t w = start >> 5;
-    const uint4* c = reinterpret_cast<const uint4*>(words) + (w >> 2);
-    q0 = ld(c); q1 = ld(c + 1); q2 = ld(c + 2);
-    p = c + 3;
-    qi = uint32_t(w & 3);
+  __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(words + (i < wlim ? i : wlim)); }
+  __device__ __forceinline__ void init(const uint32_t* wp, uint32_t lim, uint64_t start) {
+    words = wp;
+    wlim = lim;
+    w = uint32_t(start >> 5);
     const uint32_t sh = uint32_t(start & 31);
-    buf = uint64_t(word()) >> sh;
-    nb = 32 - int(sh);
-    advance();
+    buf = ((uint64_t(ld(w + 1)) << 32) | ld(w)) >> sh;
+    nb = 64 - int(sh);
+    w += 2;
+    nextw = ld(w);
   }
   __device__ __forceinline__ void refill() {   // afterwards nb >= 33
-    if (nb <= 32) { buf |= uint64_t(word()) << nb; nb += 32; advance(); }
+    const bool r = nb <= 32;
+    const uint64_t add = uint64_t(nextw) << (nb & 63);
+    buf |= r ? add : 0ull;
+    nb += r ? 32 : 0;
+    w += r ? 1u : 0u;
+    if (r) nextw = ld(w);
   }
 };
 
@@ -304,7 +302,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
-  const uint4* pmax = reinterpret_cast<const uint4*>(a.src + a.file_len - 16);
+  const uint32_t wlim = uint32_t((a.file_len - (e.payload_off + kTreeBytes)) / 4 - 1);  // last word in the file
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
     uint32_t bsz = 0, nl = 0;
@@ -338,61 +336,55 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       uint32_t si = 0, lw = 0, run = 0;
       uint64_t used = 0;
       BitIn in;
-      if (!err) in.init(words, start, pmax);
+      if (!err) in.init(words, wlim, start);
       uint64_t& buf = in.buf;
       int& nb = in.nb;
+      // one litlen symbol per iteration; a length symbol also takes its distance in the same iteration.
+      // Branch-light so the 16-32 lanes (sub-blocks) of a warp stay converged (one lookup per symbol)
       while (!err) {
         if (!last && si == nseq) break;
         in.refill();
         uint32_t ent = lut_ll[uint32_t(buf) & lmask];
         uint32_t len = ent & 15u;
-        if (len == 0) {                                 // code longer than the table index
+        if (len == 0) {                                 // code longer than the table index (cwl > 11)
           const int sym = canon_slow(buf, sm.tab[0], sm.sorted_ll, &len);
           if (sym < 0) { err = 2; break; }
           ent = ll_entry(uint32_t(sym), len);
         }
-        buf >>= len; nb -= int(len); used += len;
         const uint32_t kind = (ent >> 4) & 3u;
-        if (kind == K_LIT) {
+        const bool isl = kind == K_LEN, islit = kind == K_LIT;
+        const uint32_t xb = isl ? (ent >> 17) & 7u : 0u;
+        const uint32_t L = ((ent >> 8) & 511u) + (uint32_t(buf >> len) & ((1u << xb) - 1u));
+        const uint32_t c1 = len + xb;
+        buf >>= c1; nb -= int(c1); used += c1;
+        in.refill();
+        uint32_t de = lut_d[uint32_t(buf) & lmask];
+        uint32_t dl = de & 15u;
+        if (isl && dl == 0) {
+          const int sym = canon_slow(buf, sm.tab[1], sm.sorted_d, &dl);
+          if (sym < 0) { err = 5; break; }
+          de = d_entry(uint32_t(sym), dl);
+        }
+        if (isl && ((de >> 4) & 3u) == K_BAD) { err = 5; break; }
+        const uint32_t dx = (de >> 24) & 15u;
+        const uint32_t dist = ((de >> 8) & 0xffffu) + (uint32_t(buf >> dl) & ((1u << dx) - 1u));
+        const uint32_t c2 = isl ? dl + dx : 0u;
+        buf >>= c2; nb -= int(c2); used += c2;
+        if (islit) {
           if (lw >= nl) { err = 3; break; }
           lit[lw++] = uint8_t(ent >> 8);
-          if (++run == kMaxLitRun) {                    // R10/R16: literal-only sequence at 1023
-            if (si >= nseq) { err = 4; break; }
-            rec[si++] = kMaxLitRun;
-            run = 0;
-          }
-        } else if (kind == K_LEN) {
-          const uint32_t xb = (ent >> 17) & 7u;
-          const uint32_t L = ((ent >> 8) & 511u) + (uint32_t(buf) & ((1u << xb) - 1u));
-          buf >>= xb; nb -= int(xb); used += xb;
-          in.refill();
-          uint32_t de = lut_d[uint32_t(buf) & lmask];
-          uint32_t dl = de & 15u;
-          if (dl == 0) {
-            const int sym = canon_slow(buf, sm.tab[1], sm.sorted_d, &dl);
-            if (sym < 0) { err = 5; break; }
-            de = d_entry(uint32_t(sym), dl);
-          }
-          if (((de >> 4) & 3u) == K_BAD) { err = 5; break; }
-          buf >>= dl; nb -= int(dl); used += dl;
-          const uint32_t dx = (de >> 24) & 15u;
-          const uint32_t dist = ((de >> 8) & 0xffffu) + (uint32_t(buf) & ((1u << dx) - 1u));
-          buf >>= dx; nb -= int(dx); used += dx;
-          if (L < a.min_match || L > a.max_match || si >= nseq) { err = 6; break; }
-          rec[si++] = run | ((L - mm1) << 10) | ((dist - 1) << 16);
-          run = 0;
-        } else if (kind == K_EOB) {
-          if (!last) { err = 7; break; }
-          if (run) {
-            if (si >= nseq) { err = 4; break; }
-            rec[si++] = run;
-            run = 0;
-          }
-          break;
-        } else {
-          err = 2;
-          break;
+          ++run;
         }
+        // R10/R16: a sequence closes at a length code, at 1023 literals, or at EOB with pending literals
+        const bool close = isl || (islit && run == kMaxLitRun) || (kind == K_EOB && run != 0);
+        if (close) {
+          if (si >= nseq) { err = 4; break; }
+          rec[si++] = isl ? (run | ((L - mm1) << 10) | ((dist - 1) << 16)) : run;
+          run = 0;
+        }
+        if (isl && (L < a.min_match || L > a.max_match)) { err = 6; break; }
+        if (kind == K_EOB) { if (!last) err = 7; break; }
+        if (kind == K_BAD) { err = 2; break; }
         if (used > bsz) { err = 8; break; }
       }
       if (!err && (si != nseq || run != 0 || used != bsz || lw != nl)) err = 9;
@@ -458,6 +450,33 @@ __device__ __forceinline__ void ring_copy(uint8_t* D, uint32_t dm, uint32_t d, c
   for (uint32_t k = 0; k < n; ++k) D[(d + k) & dm] = S[(s + k) & sm];
 }
 
+// Copy n bytes into ring destination positions [d, d+n) whose slots are ZERO (see the zero frontier in
+// lz77_kernel), from source positions [s, s+n) of a ring (mask sm) that do not overlap the destination.
+// Each destination word is the funnel shift of two aligned source words; whole words are stored, partial words
+// (shared with the neighbouring segment, possibly of another lane) are OR-ed in with ATOMS.OR. No byte loops.
+__device__ __forceinline__ void ring_copy_or(uint8_t* D, uint32_t dm, uint32_t d, const uint8_t* S, uint32_t sm,
+                                             uint32_t s, uint32_t n) {
+  if (n == 0) return;
+  const uint32_t* S32 = reinterpret_cast<const uint32_t*>(S);
+  uint32_t* D32 = reinterpret_cast<uint32_t*>(D);
+  const uint32_t swm = sm >> 2, dwm = dm >> 2;
+  const uint32_t w0 = d >> 2, w1 = (d + n - 1) >> 2;
+  uint32_t sp = s - (d & 3u);                   // source byte that lands on the first destination word start
+  const uint32_t sh = (sp & 3u) * 8u;
+  uint32_t sw = sp >> 2;
+  uint32_t lo = S32[sw & swm];
+  for (uint32_t w = w0; w <= w1; ++w) {
+    const uint32_t hi = S32[(sw + 1) & swm];
+    const uint32_t v = __funnelshift_r(lo, hi, sh);
+    lo = hi;
+    ++sw;
+    const uint32_t b0 = w == w0 ? (d & 3u) : 0u, b1 = w == w1 ? ((d + n - 1) & 3u) : 3u;
+    const uint32_t m = (0xffffffffu << (8 * b0)) & (0xffffffffu >> (8 * (3 - b1)));
+    if (m == 0xffffffffu) D32[w & dwm] = v;
+    else atomicOr(&D32[w & dwm], v & m);
+  }
+}
+
 struct GlobalOut {
   uint8_t* out;
   __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { copy_nolap(out + dst, out + src, n); }
@@ -465,7 +484,7 @@ struct GlobalOut {
 struct RingOut {
   uint8_t* ring;
   uint32_t rm;
-  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy(ring, rm, dst, ring, rm, src, n); }
+  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy_or(ring, rm, dst, ring, rm, src, n); }
 };
 
 // a7 for one warp group: back-references of the lanes with has = (L > 0). Returns false on NO_PROGRESS.
@@ -587,6 +606,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const GlobalOut go{out};
 
   uint32_t o_carry = 0, l_carry = 0, flushed = 0;
+  uint32_t zf = 0;  // zero frontier (16-aligned, >= o_carry): ring slots of positions [o_carry, zf) are zero
   uint32_t rq0 = lane < n_seq ? __ldg(recs + lane) : 0u;
   uint32_t rq1 = lane + 32 < n_seq ? __ldg(recs + lane + 32) : 0u;
   uint32_t rq2 = lane + 64 < n_seq ? __ldg(recs + lane + 64) : 0u;
@@ -619,6 +639,12 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
     const bool has = act && L;
     const bool fast = out_sum + a.window + 16 <= RING && lit_sum + kLitAhead <= kLitRing;
     if (fast) {
+      // zero the ring slots of this group's output (they hold dead, already flushed bytes: RING >= window +
+      // group output), so the OR-writes of ring_copy_or assemble partial words without byte loops
+      const uint32_t zend = (o_carry + out_sum + 15u) & ~15u;
+      for (uint32_t q = (zf >> 4) + lane; q < (zend >> 4); q += 32)
+        reinterpret_cast<uint4*>(ring)[q & (RM >> 4)] = make_uint4(0u, 0u, 0u, 0u);
+      if (zend > zf) zf = zend;
       // stage the group's literals (rel range [lofs + l_carry, need)) into the literal ring
       const uint32_t need = lofs + l_carry + lit_sum;
       while (lf < need + kLitAhead && lf < lend16 && lf + kLitUnit <= lofs + l_carry + kLitRing) {
@@ -631,7 +657,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       cp_wait(issued > needed ? issued - needed : 0u);
       __syncwarp();
       // a6: literal strings into the output ring
-      if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+      if (act) ring_copy_or(ring, RM, op, lring, LM, lofs + lp, lit);
       // a7: back-references inside the ring
       if (!resolve_group<STRAT, STATS>(a, ro, lane, has, dst, src, L, op, o_carry, b, g0)) return;
       __syncwarp();
@@ -652,6 +678,8 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       const uint32_t o_new = o_carry + out_sum;
       const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
       for (uint32_t p = o_new - keep + lane; p < o_new; p += 32) ring[p & RM] = out[p];
+      zf = (o_new + 15u) & ~15u;
+      for (uint32_t p = o_new + lane; p < zf; p += 32) ring[p & RM] = 0;
       flushed = o_new;
       cp_wait(0);
       lf = ((lofs + l_carry + lit_sum) / kLitUnit) * kLitUnit;
