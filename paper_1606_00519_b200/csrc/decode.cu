@@ -126,15 +126,13 @@ struct HuffSmem {
 };
 
 // canonical walk for codes longer than the table index (cwl > lut_bits): bits are taken LSB-first from buf
-__device__ int canon_slow(uint64_t buf, const CanonTab& t, const uint16_t* sorted, uint32_t* len_out) {
+// returns symbol | length << 16, or -1 if no code matches
+__device__ int canon_slow(uint64_t buf, const CanonTab& t, const uint16_t* sorted) {
   int code = 0, first = 0, index = 0;
   for (int l = 1; l <= 15; ++l) {
     code |= int((buf >> (l - 1)) & 1u);
     const int cnt = t.count[l];
-    if (code - first < cnt) {
-      *len_out = uint32_t(l);
-      return sorted[index + code - first];
-    }
+    if (code - first < cnt) return int(sorted[index + code - first]) | (l << 16);
     index += cnt;
     first += cnt;
     first <<= 1;
@@ -160,34 +158,32 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
-// LSB-first bit reader: 64-bit buffer + the next 32-bit word already loaded, refilled branch-free (predicated)
-// so lanes decoding different sub-blocks stay converged. Sequential words of one thread hit L1 after the first
-// touch of each 128-byte line. Word indices are clamped to the file (values past the stream are never used).
+// LSB-first bit reader: a 64-bit window (lo, hi) at 32-bit granularity, a bit offset into it, and the next
+// word already loaded. peek() = one funnel shift; consume(n <= 32) advances by at most one word, branch-free
+// (the load of the following word is predicated and only needed one word later). Sequential words of one
+// thread hit L1 after the first touch of each 128-byte line. Word indices are clamped to the file.
 struct BitIn {
   const uint32_t* words;
-  uint32_t wlim;
-  uint32_t w, nextw;
-  uint64_t buf;
-  int nb;
+  uint32_t wlim, w, lo, hi, nx, pos, w0, pos0;
   __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(words + (i < wlim ? i : wlim)); }
   __device__ __forceinline__ void init(const uint32_t* wp, uint32_t lim, uint64_t start) {
     words = wp;
     wlim = lim;
-    w = uint32_t(start >> 5);
-    const uint32_t sh = uint32_t(start & 31);
-    buf = ((uint64_t(ld(w + 1)) << 32) | ld(w)) >> sh;
-    nb = 64 - int(sh);
-    w += 2;
-    nextw = ld(w);
+    w0 = uint32_t(start >> 5);
+    pos0 = pos = uint32_t(start & 31);
+    lo = ld(w0); hi = ld(w0 + 1); nx = ld(w0 + 2);
+    w = w0 + 3;
   }
-  __device__ __forceinline__ void refill() {   // afterwards nb >= 33
-    const bool r = nb <= 32;
-    const uint64_t add = uint64_t(nextw) << (nb & 63);
-    buf |= r ? add : 0ull;
-    nb += r ? 32 : 0;
-    w += r ? 1u : 0u;
-    if (r) nextw = ld(w);
+  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
+  __device__ __forceinline__ void consume(uint32_t n) {
+    pos += n;
+    const bool c = pos >= 32;
+    pos -= c ? 32u : 0u;
+    lo = c ? hi : lo;
+    hi = c ? nx : hi;
+    if (c) { nx = ld(w); ++w; }
   }
+  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0 - 3) * 32 + pos - pos0; }
 };
 
 // ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
@@ -334,60 +330,55 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       uint32_t* rec = rec_base + seq0;
       uint8_t* lit = lit_base + lstart;
       uint32_t si = 0, lw = 0, run = 0;
-      uint64_t used = 0;
       BitIn in;
-      if (!err) in.init(words, wlim, start);
-      uint64_t& buf = in.buf;
-      int& nb = in.nb;
+      in.init(words, wlim, err ? 0 : start);
       // one litlen symbol per iteration; a length symbol also takes its distance in the same iteration.
-      // Branch-light so the 16-32 lanes (sub-blocks) of a warp stay converged (one lookup per symbol)
+      // The body is branch-light (predicated stores, deferred checks) so the lanes (sub-blocks) of a warp stay
+      // converged (one table lookup per symbol).
+      uint32_t kind = K_LIT, bad = 0;
       while (!err) {
-        if (!last && si == nseq) break;
-        in.refill();
-        uint32_t ent = lut_ll[uint32_t(buf) & lmask];
+        if (!last && si >= nseq) break;
+        const uint32_t pk = in.peek();
+        uint32_t ent = lut_ll[pk & lmask];
         uint32_t len = ent & 15u;
         if (len == 0) {                                 // code longer than the table index (cwl > 11)
-          const int sym = canon_slow(buf, sm.tab[0], sm.sorted_ll, &len);
-          if (sym < 0) { err = 2; break; }
-          ent = ll_entry(uint32_t(sym), len);
+          const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
+          ent = sl < 0 ? (K_BAD << 4) | 1u : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
+          len = ent & 15u;
         }
-        const uint32_t kind = (ent >> 4) & 3u;
+        kind = (ent >> 4) & 3u;
         const bool isl = kind == K_LEN, islit = kind == K_LIT;
         const uint32_t xb = isl ? (ent >> 17) & 7u : 0u;
-        const uint32_t L = ((ent >> 8) & 511u) + (uint32_t(buf >> len) & ((1u << xb) - 1u));
-        const uint32_t c1 = len + xb;
-        buf >>= c1; nb -= int(c1); used += c1;
-        in.refill();
-        uint32_t de = lut_d[uint32_t(buf) & lmask];
+        const uint32_t L = ((ent >> 8) & 511u) + ((pk >> len) & ((1u << xb) - 1u));
+        in.consume(len + xb);
+        const uint32_t pd = in.peek();
+        uint32_t de = lut_d[pd & lmask];
         uint32_t dl = de & 15u;
         if (isl && dl == 0) {
-          const int sym = canon_slow(buf, sm.tab[1], sm.sorted_d, &dl);
-          if (sym < 0) { err = 5; break; }
-          de = d_entry(uint32_t(sym), dl);
+          const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
+          de = sl < 0 ? (K_BAD << 4) : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
+          dl = de & 15u;
         }
-        if (isl && ((de >> 4) & 3u) == K_BAD) { err = 5; break; }
         const uint32_t dx = (de >> 24) & 15u;
-        const uint32_t dist = ((de >> 8) & 0xffffu) + (uint32_t(buf >> dl) & ((1u << dx) - 1u));
-        const uint32_t c2 = isl ? dl + dx : 0u;
-        buf >>= c2; nb -= int(c2); used += c2;
-        if (islit) {
-          if (lw >= nl) { err = 3; break; }
-          lit[lw++] = uint8_t(ent >> 8);
-          ++run;
-        }
+        const uint32_t dist = ((de >> 8) & 0xffffu) + ((pd >> dl) & ((1u << dx) - 1u));
+        in.consume(isl ? dl + dx : 0u);
+        if (islit && lw < nl) lit[lw] = uint8_t(ent >> 8);
+        lw += islit ? 1u : 0u;
+        run += islit ? 1u : 0u;
         // R10/R16: a sequence closes at a length code, at 1023 literals, or at EOB with pending literals
         const bool close = isl || (islit && run == kMaxLitRun) || (kind == K_EOB && run != 0);
-        if (close) {
-          if (si >= nseq) { err = 4; break; }
-          rec[si++] = isl ? (run | ((L - mm1) << 10) | ((dist - 1) << 16)) : run;
-          run = 0;
-        }
-        if (isl && (L < a.min_match || L > a.max_match)) { err = 6; break; }
-        if (kind == K_EOB) { if (!last) err = 7; break; }
-        if (kind == K_BAD) { err = 2; break; }
-        if (used > bsz) { err = 8; break; }
+        if (close && si < nseq) rec[si] = isl ? (run | ((L - mm1) << 10) | ((dist - 1) << 16)) : run;
+        si += close ? 1u : 0u;
+        run = close ? 0u : run;
+        bad |= isl && (L < a.min_match || L > a.max_match || ((de >> 4) & 3u) == K_BAD || dl == 0);
+        if (kind >= K_EOB || lw > nl || si > nseq) break;
       }
-      if (!err && (si != nseq || run != 0 || used != bsz || lw != nl)) err = 9;
+      if (!err) {
+        if (bad) err = 6;
+        else if (kind == K_BAD) err = 2;
+        else if (kind == K_EOB && !last) err = 7;
+        else if (si != nseq || run != 0 || lw != nl || in.consumed() != bsz) err = 9;
+      }
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
   }
@@ -405,6 +396,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
 constexpr uint32_t kLitRing = 2048;
 constexpr uint32_t kLitUnit = 512;   // 32 lanes x 16 B per cp.async instruction
 constexpr uint32_t kLitAhead = 1024; // prefetch distance in literal bytes
+constexpr uint32_t kPrmBytes = 32 * 16;  // per-warp table of the group's 32 sequence descriptors (DE pass)
 
 // byte-granular copy without overlap (dist >= L, reading R2), global memory (slow path)
 __device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_t n) {
@@ -450,33 +442,6 @@ __device__ __forceinline__ void ring_copy(uint8_t* D, uint32_t dm, uint32_t d, c
   for (uint32_t k = 0; k < n; ++k) D[(d + k) & dm] = S[(s + k) & sm];
 }
 
-// Copy n bytes into ring destination positions [d, d+n) whose slots are ZERO (see the zero frontier in
-// lz77_kernel), from source positions [s, s+n) of a ring (mask sm) that do not overlap the destination.
-// Each destination word is the funnel shift of two aligned source words; whole words are stored, partial words
-// (shared with the neighbouring segment, possibly of another lane) are OR-ed in with ATOMS.OR. No byte loops.
-__device__ __forceinline__ void ring_copy_or(uint8_t* D, uint32_t dm, uint32_t d, const uint8_t* S, uint32_t sm,
-                                             uint32_t s, uint32_t n) {
-  if (n == 0) return;
-  const uint32_t* S32 = reinterpret_cast<const uint32_t*>(S);
-  uint32_t* D32 = reinterpret_cast<uint32_t*>(D);
-  const uint32_t swm = sm >> 2, dwm = dm >> 2;
-  const uint32_t w0 = d >> 2, w1 = (d + n - 1) >> 2;
-  uint32_t sp = s - (d & 3u);                   // source byte that lands on the first destination word start
-  const uint32_t sh = (sp & 3u) * 8u;
-  uint32_t sw = sp >> 2;
-  uint32_t lo = S32[sw & swm];
-  for (uint32_t w = w0; w <= w1; ++w) {
-    const uint32_t hi = S32[(sw + 1) & swm];
-    const uint32_t v = __funnelshift_r(lo, hi, sh);
-    lo = hi;
-    ++sw;
-    const uint32_t b0 = w == w0 ? (d & 3u) : 0u, b1 = w == w1 ? ((d + n - 1) & 3u) : 3u;
-    const uint32_t m = (0xffffffffu << (8 * b0)) & (0xffffffffu >> (8 * (3 - b1)));
-    if (m == 0xffffffffu) D32[w & dwm] = v;
-    else atomicOr(&D32[w & dwm], v & m);
-  }
-}
-
 struct GlobalOut {
   uint8_t* out;
   __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { copy_nolap(out + dst, out + src, n); }
@@ -484,7 +449,7 @@ struct GlobalOut {
 struct RingOut {
   uint8_t* ring;
   uint32_t rm;
-  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy_or(ring, rm, dst, ring, rm, src, n); }
+  __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy(ring, rm, dst, ring, rm, src, n); }
 };
 
 // a7 for one warp group: back-references of the lanes with has = (L > 0). Returns false on NO_PROGRESS.
@@ -567,6 +532,70 @@ __device__ __forceinline__ void cp_wait(uint32_t allowed) {
   else asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
+// DE group, word-parallel (a6 + a7 fused). Group-relative positions xr in [0, T) (T = group output bytes).
+// Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte xr is lring[xr + ld_i], match
+// part [dst_i, opr_{i+1}) whose byte xr is (own_i ? lring : ring)[xr + md_i] (own_i: source inside its own
+// literal, reading R4). Each lane assembles whole aligned 32-bit words of the ring: owner of the word's first
+// byte by a 5-step shuffle binary search on opr, descriptors of the owner and its successor from shared memory,
+// then either one funnel-shifted word from a single contiguous source (common case) or a byte-wise gather
+// (word straddling a segment boundary). Bytes of the first word that precede the group are kept from the ring
+// (final); bytes past the group in the last word are rewritten by the next group.
+__device__ __forceinline__ uint32_t ld_word_at(const uint8_t* base, uint32_t mask, uint32_t p) {
+  const uint32_t* W = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t wm = mask >> 2, i = p >> 2;
+  return __funnelshift_r(W[i & wm], W[(i + 1) & wm], (p & 3u) * 8u);
+}
+__device__ __forceinline__ void de_group_words(uint8_t* ring, uint32_t RM, const uint8_t* lring, uint32_t LM,
+                                               uint4* prm, uint32_t lane, bool act, bool has, uint32_t opr,
+                                               uint32_t lit, uint32_t lpos, uint32_t dist, bool own, uint32_t o,
+                                               uint32_t T) {
+  const uint32_t dstr = opr + lit;
+  const uint32_t ld = lpos - opr;                                  // lring position = xr + ld
+  const uint32_t md = own ? ld - dist : o - dist;                  // match source position = xr + md
+  prm[lane] = make_uint4(opr, dstr | ((has && own) ? 0x80000000u : 0u), ld, md);
+  __syncwarp();
+  const uint32_t ob = o & 3u, nwords = (ob + T + 3) >> 2, wbase = o >> 2, RWM = RM >> 2;
+  uint32_t* R32 = reinterpret_cast<uint32_t*>(ring);
+  for (uint32_t k = lane; k < nwords; k += 32) {
+    const int32_t x0 = int32_t(4 * k) - int32_t(ob);
+    const uint32_t xs = x0 < 0 ? 0u : uint32_t(x0);
+    uint32_t j = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+      const uint32_t c = j + step;
+      const uint32_t v = __shfl_sync(FULL, opr, c);
+      j = v <= xs ? c : j;
+    }
+    const uint4 P = prm[j];
+    const uint4 Q = prm[j < 31 ? j + 1 : 31];
+    const uint32_t nstart = j < 31 ? Q.x : T;
+    const uint32_t pdst = P.y & 0x7fffffffu;
+    const uint32_t xe = min(uint32_t(x0 + 4), T);                  // exclusive end of the word inside the group
+    uint32_t val;
+    if (x0 >= 0 && xe <= nstart && (xe <= pdst || xs >= pdst)) {
+      const bool in_lit = xe <= pdst;
+      const bool from_lring = in_lit || (P.y >> 31);
+      const uint32_t p = xs + (in_lit ? P.z : P.w);
+      val = from_lring ? ld_word_at(lring, LM, p) : ld_word_at(ring, RM, p);
+    } else {
+      val = x0 < 0 ? R32[(wbase + k) & RWM] : 0u;
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const int32_t xr = x0 + bb;
+        if (xr < 0 || uint32_t(xr) >= T) continue;
+        const uint4& D = uint32_t(xr) < nstart ? P : Q;
+        const uint32_t ddst = D.y & 0x7fffffffu;
+        const bool in_lit = uint32_t(xr) < ddst;
+        const uint32_t p = uint32_t(xr) + (in_lit ? D.z : D.w);
+        const uint32_t byte = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
+        val = (val & ~(0xffu << (8 * bb))) | (byte << (8 * bb));
+      }
+    }
+    R32[(wbase + k) & RWM] = val;
+  }
+  (void)act;
+}
+
 template <int STRAT, bool STATS>
 __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t lz_smem[];
@@ -574,8 +603,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wi >= a.n_blocks) return;
   const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLitRing - 1;
-  uint8_t* ring = lz_smem + (threadIdx.x >> 5) * (RING + kLitRing);
+  uint8_t* ring = lz_smem + (threadIdx.x >> 5) * (RING + kLitRing + kPrmBytes);
   uint8_t* lring = ring + RING;
+  uint4* prm = reinterpret_cast<uint4*>(lring + kLitRing);
   const uint32_t b = a.first_block + wi;
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
@@ -606,7 +636,6 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const GlobalOut go{out};
 
   uint32_t o_carry = 0, l_carry = 0, flushed = 0;
-  uint32_t zf = 0;  // zero frontier (16-aligned, >= o_carry): ring slots of positions [o_carry, zf) are zero
   uint32_t rq0 = lane < n_seq ? __ldg(recs + lane) : 0u;
   uint32_t rq1 = lane + 32 < n_seq ? __ldg(recs + lane + 32) : 0u;
   uint32_t rq2 = lane + 64 < n_seq ? __ldg(recs + lane + 64) : 0u;
@@ -639,12 +668,6 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
     const bool has = act && L;
     const bool fast = out_sum + a.window + 16 <= RING && lit_sum + kLitAhead <= kLitRing;
     if (fast) {
-      // zero the ring slots of this group's output (they hold dead, already flushed bytes: RING >= window +
-      // group output), so the OR-writes of ring_copy_or assemble partial words without byte loops
-      const uint32_t zend = (o_carry + out_sum + 15u) & ~15u;
-      for (uint32_t q = (zf >> 4) + lane; q < (zend >> 4); q += 32)
-        reinterpret_cast<uint4*>(ring)[q & (RM >> 4)] = make_uint4(0u, 0u, 0u, 0u);
-      if (zend > zf) zf = zend;
       // stage the group's literals (rel range [lofs + l_carry, need)) into the literal ring
       const uint32_t need = lofs + l_carry + lit_sum;
       while (lf < need + kLitAhead && lf < lend16 && lf + kLitUnit <= lofs + l_carry + kLitRing) {
@@ -656,10 +679,37 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       const uint32_t issued = lf / kLitUnit, needed = (need + kLitUnit - 1) / kLitUnit;
       cp_wait(issued > needed ? issued - needed : 0u);
       __syncwarp();
-      // a6: literal strings into the output ring
-      if (act) ring_copy_or(ring, RM, op, lring, LM, lofs + lp, lit);
-      // a7: back-references inside the ring
-      if (!resolve_group<STRAT, STATS>(a, ro, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+      bool done = false;
+      if (STRAT == GOMP_STRAT_DE) {
+        // DE rule (FORMAT.md §4): every source lies below the group start (final in the ring) or in the lane's
+        // own literal string (final in the literal ring), so every output byte of the group is a function of
+        // on-chip data that no lane of this group writes: a6 and a7 become ONE word-parallel pass, balanced
+        // over the lanes (each lane assembles whole 32-bit output words), with no inter-lane ordering at all.
+        const bool de_ok = !has || src + L <= o_carry || src >= op;
+        if (__all_sync(FULL, de_ok)) {
+          de_group_words(ring, RM, lring, LM, prm, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
+                         o_carry, out_sum);
+          if (STATS) {
+            const uint32_t any = __ballot_sync(FULL, has);
+            uint32_t bytes = has ? L : 0u;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+            if (lane == 0) {
+              atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
+              if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
+            }
+          }
+          done = true;
+        } else if (STATS && lane == 0) {
+          atomicAdd(stats_ptr(a) + 66, 1ull);
+        }
+      }
+      if (!done) {
+        // a6: literal strings into the output ring; a7: back-references inside the ring (MRR / SC)
+        if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+        constexpr int S2 = STRAT == GOMP_STRAT_DE ? GOMP_STRAT_MRR : STRAT;
+        if (!resolve_group<S2, STATS>(a, ro, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+      }
       __syncwarp();
       // flush completed 16-byte chunks to HBM (coalesced 16-byte stores)
       const uint32_t q1 = (o_carry + out_sum) >> 4;
@@ -678,8 +728,6 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       const uint32_t o_new = o_carry + out_sum;
       const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
       for (uint32_t p = o_new - keep + lane; p < o_new; p += 32) ring[p & RM] = out[p];
-      zf = (o_new + 15u) & ~15u;
-      for (uint32_t p = o_new + lane; p < zf; p += 32) ring[p & RM] = 0;
       flushed = o_new;
       cp_wait(0);
       lf = ((lofs + l_carry + lit_sum) / kLitUnit) * kLitUnit;
@@ -700,7 +748,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   for (uint32_t p = max(q1 * 16, flushed) + lane; p < o_carry; p += 32) out[p] = ring[p & RM];
 }
 
-size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * (ring + kLitRing); }
+size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * (ring + kLitRing + kPrmBytes); }
 
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {

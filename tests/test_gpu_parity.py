@@ -175,7 +175,7 @@ def test_device_errors_bit_fuzz():
         _gpu(bad)
     assert e.value.name in ("HEADER_INCONSISTENT", "CORRUPT_STREAM") and e.value.block == 0
     bad = c.copy()
-    bad[64 + 24] += 1  # S of block 0: n_sub no longer ceil(n_seq / S)
+    bad[64 + 28] += 1  # n_sub of block 0: no longer ceil(n_seq / S)
     with pytest.raises(gomp.GompError) as e:
         _gpu(bad)
     assert e.value.name == "HEADER_INCONSISTENT" and e.value.block == 0
