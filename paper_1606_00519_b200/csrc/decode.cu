@@ -556,7 +556,8 @@ __device__ __forceinline__ void de_group_words(uint8_t* ring, uint32_t RM, const
   __syncwarp();
   const uint32_t ob = o & 3u, nwords = (ob + T + 3) >> 2, wbase = o >> 2, RWM = RM >> 2;
   uint32_t* R32 = reinterpret_cast<uint32_t*>(ring);
-  for (uint32_t k = lane; k < nwords; k += 32) {
+  for (uint32_t k0 = 0; k0 < nwords; k0 += 32) {   // warp-uniform trip count: the shuffles need all lanes
+    const uint32_t k = k0 + lane;
     const int32_t x0 = int32_t(4 * k) - int32_t(ob);
     const uint32_t xs = x0 < 0 ? 0u : uint32_t(x0);
     uint32_t j = 0;
@@ -566,6 +567,7 @@ __device__ __forceinline__ void de_group_words(uint8_t* ring, uint32_t RM, const
       const uint32_t v = __shfl_sync(FULL, opr, c);
       j = v <= xs ? c : j;
     }
+    if (k >= nwords) continue;
     const uint4 P = prm[j];
     const uint4 Q = prm[j < 31 ? j + 1 : 31];
     const uint32_t nstart = j < 31 ? Q.x : T;
@@ -661,8 +663,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
     const bool bad_rec = act && !mcode && (r >> 16);
     const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
     const bool bad_sz = o_carry + out_sum > ulen || l_carry + lit_sum > e.n_lit;
-    if (__any_sync(FULL, bad_ref || bad_rec) || bad_sz) {
-      if (lane == 0) report(a, bad_sz || __any_sync(FULL, bad_rec) ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g0);
+    const bool any_rec = __any_sync(FULL, bad_rec);
+    if (__any_sync(FULL, bad_ref) || any_rec || bad_sz) {
+      if (lane == 0) report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g0);
       return;
     }
     const bool has = act && L;
