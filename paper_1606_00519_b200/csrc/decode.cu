@@ -532,70 +532,38 @@ __device__ __forceinline__ void cp_wait(uint32_t allowed) {
   else asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-// DE group, word-parallel (a6 + a7 fused). Group-relative positions xr in [0, T) (T = group output bytes).
-// Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte xr is lring[xr + ld_i], match
-// part [dst_i, opr_{i+1}) whose byte xr is (own_i ? lring : ring)[xr + md_i] (own_i: source inside its own
-// literal, reading R4). Each lane assembles whole aligned 32-bit words of the ring: owner of the word's first
-// byte by a 5-step shuffle binary search on opr, descriptors of the owner and its successor from shared memory,
-// then either one funnel-shifted word from a single contiguous source (common case) or a byte-wise gather
-// (word straddling a segment boundary). Bytes of the first word that precede the group are kept from the ring
-// (final); bytes past the group in the last word are rewritten by the next group.
-__device__ __forceinline__ uint32_t ld_word_at(const uint8_t* base, uint32_t mask, uint32_t p) {
-  const uint32_t* W = reinterpret_cast<const uint32_t*>(base);
-  const uint32_t wm = mask >> 2, i = p >> 2;
-  return __funnelshift_r(W[i & wm], W[(i + 1) & wm], (p & 3u) * 8u);
-}
-__device__ __forceinline__ void de_group_words(uint8_t* ring, uint32_t RM, const uint8_t* lring, uint32_t LM,
-                                               uint4* prm, uint32_t lane, bool act, bool has, uint32_t opr,
-                                               uint32_t lit, uint32_t lpos, uint32_t dist, bool own, uint32_t o,
-                                               uint32_t T) {
+// DE group as byte rows (a6 + a7 fused). Group-relative positions x in [0, T) (T = group output bytes).
+// Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte x is lring[x + ld_i], match part
+// [dst_i, opr_{i+1}) whose byte x is (own_i ? lring : ring)[x + md_i] (own_i: source inside its own literal,
+// reading R4). Under the DE rule no source lies in this group's output, so the group is computed in rows of
+// 32 consecutive bytes, lane t owning byte base + t: the owner sequence comes from a one-instruction OR-vote of
+// the row's sequence starts (REDUX) and a popcount; its descriptor is one broadcast 16-byte shared load.
+// Uniform control flow, no divergence, no inter-lane ordering (P:295-329 taken to byte granularity).
+__device__ __forceinline__ void de_group_rows(uint8_t* ring, uint32_t RM, const uint8_t* lring, uint32_t LM,
+                                              uint4* prm, uint32_t lane, bool act, bool has, uint32_t opr,
+                                              uint32_t lit, uint32_t lpos, uint32_t dist, bool own, uint32_t o,
+                                              uint32_t T) {
   const uint32_t dstr = opr + lit;
-  const uint32_t ld = lpos - opr;                                  // lring position = xr + ld
-  const uint32_t md = own ? ld - dist : o - dist;                  // match source position = xr + md
+  const uint32_t ld = lpos - opr;                                  // lring position of byte x = x + ld
+  const uint32_t md = (has && own) ? ld - dist : o - dist;         // match source position = x + md
   prm[lane] = make_uint4(opr, dstr | ((has && own) ? 0x80000000u : 0u), ld, md);
   __syncwarp();
-  const uint32_t ob = o & 3u, nwords = (ob + T + 3) >> 2, wbase = o >> 2, RWM = RM >> 2;
-  uint32_t* R32 = reinterpret_cast<uint32_t*>(ring);
-  for (uint32_t k0 = 0; k0 < nwords; k0 += 32) {   // warp-uniform trip count: the shuffles need all lanes
-    const uint32_t k = k0 + lane;
-    const int32_t x0 = int32_t(4 * k) - int32_t(ob);
-    const uint32_t xs = x0 < 0 ? 0u : uint32_t(x0);
-    uint32_t j = 0;
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1) {
-      const uint32_t c = j + step;
-      const uint32_t v = __shfl_sync(FULL, opr, c);
-      j = v <= xs ? c : j;
+  const uint32_t le = (2u << lane) - 1u;                           // lanes <= this lane
+  uint32_t c0 = 0;                                                 // sequences starting before the row
+  for (uint32_t base = 0; base < T; base += 32) {
+    const uint32_t rel = opr - base;
+    const uint32_t M = __reduce_or_sync(FULL, (act && rel < 32u) ? (1u << rel) : 0u);
+    const uint32_t j = c0 + __popc(M & le) - 1u;
+    c0 += __popc(M);
+    const uint32_t x = base + lane;
+    if (x < T) {
+      const uint4 D = prm[j];
+      const bool in_lit = x < (D.y & 0x7fffffffu);
+      const uint32_t p = x + (in_lit ? D.z : D.w);
+      const uint32_t byte = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
+      ring[(o + x) & RM] = uint8_t(byte);
     }
-    if (k >= nwords) continue;
-    const uint4 P = prm[j];
-    const uint4 Q = prm[j < 31 ? j + 1 : 31];
-    const uint32_t nstart = j < 31 ? Q.x : T;
-    const uint32_t pdst = P.y & 0x7fffffffu;
-    const uint32_t xe = min(uint32_t(x0 + 4), T);                  // exclusive end of the word inside the group
-    uint32_t val;
-    if (x0 >= 0 && xe <= nstart && (xe <= pdst || xs >= pdst)) {
-      const bool in_lit = xe <= pdst;
-      const bool from_lring = in_lit || (P.y >> 31);
-      const uint32_t p = xs + (in_lit ? P.z : P.w);
-      val = from_lring ? ld_word_at(lring, LM, p) : ld_word_at(ring, RM, p);
-    } else {
-      val = x0 < 0 ? R32[(wbase + k) & RWM] : 0u;
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb) {
-        const int32_t xr = x0 + bb;
-        if (xr < 0 || uint32_t(xr) >= T) continue;
-        const uint4& D = uint32_t(xr) < nstart ? P : Q;
-        const uint32_t ddst = D.y & 0x7fffffffu;
-        const bool in_lit = uint32_t(xr) < ddst;
-        const uint32_t p = uint32_t(xr) + (in_lit ? D.z : D.w);
-        const uint32_t byte = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
-        val = (val & ~(0xffu << (8 * bb))) | (byte << (8 * bb));
-      }
-    }
-    R32[(wbase + k) & RWM] = val;
   }
-  (void)act;
 }
 
 template <int STRAT, bool STATS>
@@ -686,12 +654,12 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       if (STRAT == GOMP_STRAT_DE) {
         // DE rule (FORMAT.md §4): every source lies below the group start (final in the ring) or in the lane's
         // own literal string (final in the literal ring), so every output byte of the group is a function of
-        // on-chip data that no lane of this group writes: a6 and a7 become ONE word-parallel pass, balanced
-        // over the lanes (each lane assembles whole 32-bit output words), with no inter-lane ordering at all.
+        // on-chip data that no lane of this group writes: a6 and a7 become ONE byte-parallel pass over the
+        // group's output rows, balanced over the lanes, with no inter-lane ordering at all.
         const bool de_ok = !has || src + L <= o_carry || src >= op;
         if (__all_sync(FULL, de_ok)) {
-          de_group_words(ring, RM, lring, LM, prm, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
-                         o_carry, out_sum);
+          de_group_rows(ring, RM, lring, LM, prm, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
+                        o_carry, out_sum);
           if (STATS) {
             const uint32_t any = __ballot_sync(FULL, has);
             uint32_t bytes = has ? L : 0u;
