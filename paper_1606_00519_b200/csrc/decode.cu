@@ -158,32 +158,34 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
-// LSB-first bit reader: a 64-bit window (lo, hi) at 32-bit granularity, a bit offset into it, and the next
-// word already loaded. peek() = one funnel shift; consume(n <= 32) advances by at most one word, branch-free
-// (the load of the following word is predicated and only needed one word later). Sequential words of one
-// thread hit L1 after the first touch of each 128-byte line. Word indices are clamped to the file.
+// LSB-first bit reader: a 64-bit window (lo, hi) at 32-bit granularity, a bit offset into it, and a queue of
+// the next three words already loaded. peek() = one funnel shift; consume(n <= 32) advances by at most one
+// word, branch-free. A loaded word is first read (moved down the queue) three word-crossings after its load
+// is issued, so the global-load latency never sits on the per-symbol dependency chain (an instruction that
+// reads a register still waits for its load even when predicated off). Word indices are clamped to the file.
 struct BitIn {
   const uint32_t* words;
-  uint32_t wlim, w, lo, hi, nx, pos, w0, pos0;
+  uint32_t wlim, w, lo, hi, n1, n2, n3, pos, w0, pos0;
   __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(words + (i < wlim ? i : wlim)); }
   __device__ __forceinline__ void init(const uint32_t* wp, uint32_t lim, uint64_t start) {
     words = wp;
     wlim = lim;
     w0 = uint32_t(start >> 5);
     pos0 = pos = uint32_t(start & 31);
-    lo = ld(w0); hi = ld(w0 + 1); nx = ld(w0 + 2);
-    w = w0 + 3;
+    lo = ld(w0); hi = ld(w0 + 1); n1 = ld(w0 + 2); n2 = ld(w0 + 3); n3 = ld(w0 + 4);
+    w = w0 + 5;
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
   __device__ __forceinline__ void consume(uint32_t n) {
     pos += n;
-    const bool c = pos >= 32;
-    pos -= c ? 32u : 0u;
-    lo = c ? hi : lo;
-    hi = c ? nx : hi;
-    if (c) { nx = ld(w); ++w; }
+    if (pos >= 32) {
+      pos -= 32;
+      lo = hi; hi = n1; n1 = n2; n2 = n3;
+      n3 = ld(w);
+      ++w;
+    }
   }
-  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0 - 3) * 32 + pos - pos0; }
+  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0 - 5) * 32 + pos - pos0; }
 };
 
 // ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
@@ -550,18 +552,30 @@ __device__ __forceinline__ void de_group_rows(uint8_t* ring, uint32_t RM, const 
   __syncwarp();
   const uint32_t le = (2u << lane) - 1u;                           // lanes <= this lane
   uint32_t c0 = 0;                                                 // sequences starting before the row
-  for (uint32_t base = 0; base < T; base += 32) {
-    const uint32_t rel = opr - base;
-    const uint32_t M = __reduce_or_sync(FULL, (act && rel < 32u) ? (1u << rel) : 0u);
-    const uint32_t j = c0 + __popc(M & le) - 1u;
-    c0 += __popc(M);
-    const uint32_t x = base + lane;
-    if (x < T) {
-      const uint4 D = prm[j];
-      const bool in_lit = x < (D.y & 0x7fffffffu);
-      const uint32_t p = x + (in_lit ? D.z : D.w);
-      const uint32_t byte = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
-      ring[(o + x) & RM] = uint8_t(byte);
+  // four rows per step: all loads of a step issue before its stores (sources never lie in this group's
+  // output, so the stores cannot alias them) to keep the shared-memory latency off the serial chain
+  for (uint32_t base0 = 0; base0 < T; base0 += 128) {
+    uint32_t byte[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t base = base0 + 32 * r;
+      const uint32_t rel = opr - base;
+      const uint32_t M = __reduce_or_sync(FULL, (act && rel < 32u) ? (1u << rel) : 0u);
+      const uint32_t j = c0 + __popc(M & le) - 1u;
+      c0 += __popc(M);
+      const uint32_t x = base + lane;
+      byte[r] = 0;
+      if (x < T) {
+        const uint4 D = prm[j];
+        const bool in_lit = x < (D.y & 0x7fffffffu);
+        const uint32_t p = x + (in_lit ? D.z : D.w);
+        byte[r] = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t x = base0 + 32 * r + lane;
+      if (x < T) ring[(o + x) & RM] = uint8_t(byte[r]);
     }
   }
 }
