@@ -158,43 +158,71 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
-// LSB-first bit reader: a 64-bit window (lo, hi) at 32-bit granularity, a bit offset into it, and a queue of
-// the next three words already loaded. peek() = one funnel shift; consume(n <= 32) advances by at most one
-// word, branch-free. A loaded word is first read (moved down the queue) three word-crossings after its load
-// is issued, so the global-load latency never sits on the per-symbol dependency chain (an instruction that
-// reads a register still waits for its load even when predicated off). Word indices are clamped to the file.
-struct BitIn {
-  const uint32_t* words;
-  uint32_t wlim, w, lo, hi, n1, n2, n3, pos, w0, pos0;
-  __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(words + (i < wlim ? i : wlim)); }
-  __device__ __forceinline__ void init(const uint32_t* wp, uint32_t lim, uint64_t start) {
-    words = wp;
-    wlim = lim;
-    w0 = uint32_t(start >> 5);
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// LSB-first bit reader of one sub-block. The thread's bitstream is staged through its own 8 x 16-byte ring in
+// shared memory by cp.async (LDGSTS), issued 6-7 chunks (~100 bits x 7) ahead of use, so no global-load latency
+// sits on the per-symbol dependency chain. The current 64-bit window is two registers (lo, hi) and a bit
+// offset: peek() = one funnel shift; consume(n <= 32) crosses at most one word, which costs one shared load.
+// Chunk addresses are clamped to the file (bytes past the stream are never used).
+struct BitRing {
+  const uint32_t* ring;  // this thread's 32-word ring (shared memory)
+  uint32_t ring_s;       // its shared-window address for cp.async
+  const uint8_t* gbase;  // 16-aligned start of the block's bitstream
+  uint64_t gmax;         // last valid 16-byte chunk offset from gbase
+  uint32_t w, w0, lo, hi, pos, pos0, c0;
+  __device__ __forceinline__ void issue(uint32_t c) {
+    const uint64_t off = uint64_t(c) * 16u;
+    cp_async16(ring_s + (c & 7u) * 16u, gbase + (off <= gmax ? off : gmax));
+    cp_commit();
+  }
+  __device__ __forceinline__ void init(const uint32_t* r, const uint8_t* gb, uint64_t gm, uint64_t start) {
+    ring = r;
+    ring_s = uint32_t(__cvta_generic_to_shared(r));
+    gbase = gb;
+    gmax = gm;
+    w0 = w = uint32_t(start >> 5);
     pos0 = pos = uint32_t(start & 31);
-    lo = ld(w0); hi = ld(w0 + 1); n1 = ld(w0 + 2); n2 = ld(w0 + 3); n3 = ld(w0 + 4);
-    w = w0 + 5;
+    c0 = w0 >> 2;
+#pragma unroll
+    for (uint32_t k = 0; k < 7; ++k) issue(c0 + k);
+    cp_wait_n<6>();                                  // chunk c0 landed
+    if ((w0 & 3u) == 3u) { issue(c0 + 7); cp_wait_n<6>(); }   // hi lies in chunk c0 + 1
+    lo = ring[w0 & 31u];
+    hi = ring[(w0 + 1) & 31u];
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
   __device__ __forceinline__ void consume(uint32_t n) {
     pos += n;
     if (pos >= 32) {
       pos -= 32;
-      lo = hi; hi = n1; n1 = n2; n2 = n3;
-      n3 = ld(w);
       ++w;
+      lo = hi;
+      const uint32_t nw = w + 1;
+      if ((nw & 3u) == 0) {                          // entering chunk nw/4: top up the ring, wait for it
+        issue((nw >> 2) + 6);
+        cp_wait_n<6>();
+      }
+      hi = ring[nw & 31u];
     }
   }
-  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0 - 5) * 32 + pos - pos0; }
+  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0) * 32 + pos - pos0; }
 };
 
 // ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
+template <bool LONG>   // LONG: cwl > lut_bits, codes longer than the table index take the canonical walk
 __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
   const uint32_t lut_n = 1u << a.lut_bits;
   uint32_t* lut_d = lut_ll + lut_n;
+  uint32_t* bit_rings = lut_d + lut_n;                  // 32 words per thread
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
@@ -279,7 +307,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
     const uint32_t idx = i - (t ? lut_n : 0u);
     const uint32_t v = __brev(idx) >> (32 - LB);      // code bits, first stream bit most significant
     const CanonTab& T = sm.tab[t];
-    uint32_t ent = 0;                                  // 0 = unresolved (long code or invalid)
+    uint32_t ent = LONG ? 0u : ((K_BAD << 4) | 1u);    // unresolved: long code (LONG) or invalid
     for (uint32_t l = 1; l <= LB; ++l) {
       const uint32_t code = v >> (LB - l);
       if (code - T.first[l] < T.count[l]) {
@@ -293,14 +321,13 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   __syncthreads();
 
   // a2 + a4: sub-blocks in chunks of blockDim; CTA-wide exclusive scans give start bit and literal offset
-  const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + kTreeBytes);
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint8_t* subt = a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total;
   uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
-  const uint32_t wlim = uint32_t((a.file_len - (e.payload_off + kTreeBytes)) / 4 - 1);  // last word in the file
+  const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);  // last in-file 16-byte chunk offset
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
     uint32_t bsz = 0, nl = 0;
@@ -332,8 +359,8 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       uint32_t* rec = rec_base + seq0;
       uint8_t* lit = lit_base + lstart;
       uint32_t si = 0, lw = 0, run = 0;
-      BitIn in;
-      in.init(words, wlim, err ? 0 : start);
+      BitRing in;
+      in.init(bit_rings + 32 * tid, pl + kTreeBytes, gmax, err ? 0 : start);
       // one litlen symbol per iteration; a length symbol also takes its distance in the same iteration.
       // The body is branch-light (predicated stores, deferred checks) so the lanes (sub-blocks) of a warp stay
       // converged (one table lookup per symbol).
@@ -343,7 +370,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
         const uint32_t pk = in.peek();
         uint32_t ent = lut_ll[pk & lmask];
         uint32_t len = ent & 15u;
-        if (len == 0) {                                 // code longer than the table index (cwl > 11)
+        if (LONG && len == 0) {                         // code longer than the table index (cwl > 11)
           const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
           ent = sl < 0 ? (K_BAD << 4) | 1u : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
           len = ent & 15u;
@@ -356,7 +383,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
         const uint32_t pd = in.peek();
         uint32_t de = lut_d[pd & lmask];
         uint32_t dl = de & 15u;
-        if (isl && dl == 0) {
+        if (LONG && isl && dl == 0) {
           const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
           de = sl < 0 ? (K_BAD << 4) : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
           dl = de & 15u;
@@ -383,6 +410,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       }
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
+    cp_wait_n<0>();
   }
   __syncthreads();
   if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
@@ -524,10 +552,6 @@ __device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint3
   return true;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait(uint32_t allowed) {
   if (allowed >= 2) asm volatile("cp.async.wait_group 2;\n" ::);
   else if (allowed == 1) asm volatile("cp.async.wait_group 1;\n" ::);
@@ -748,8 +772,8 @@ void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
   }
 }
 
-size_t huff_smem_bytes(uint32_t lut_bits) {
-  return ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << lut_bits) * sizeof(uint32_t);
+size_t huff_smem_bytes(uint32_t lut_bits, uint32_t nt) {
+  return ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << lut_bits) * sizeof(uint32_t) + size_t(nt) * 128;
 }
 
 gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
@@ -806,8 +830,14 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     // CTA size ~ sub-blocks per block (thread per sub-block), 32..256
     const uint64_t avg = (uint64_t(info->n_sub_total) + info->n_blocks - 1) / std::max<uint32_t>(info->n_blocks, 1);
     uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg + 31) / 32 * 32)));
-    const size_t smem = huff_smem_bytes(a.lut_bits);
-    huff_decode_kernel<<<nblk, nt, smem, st>>>(a);
+    const size_t smem = huff_smem_bytes(a.lut_bits, nt);
+    if (info->cwl > a.lut_bits) {
+      cudaFuncSetAttribute(huff_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      huff_decode_kernel<true><<<nblk, nt, smem, st>>>(a);
+    } else {
+      cudaFuncSetAttribute(huff_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      huff_decode_kernel<false><<<nblk, nt, smem, st>>>(a);
+    }
     if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
   }
   switch (s) {
