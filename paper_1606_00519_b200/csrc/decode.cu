@@ -158,12 +158,31 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, uint32_t lane
   return v;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+// explicit shared-window accesses (32-bit addresses): keeps generic->shared conversions out of hot loops
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v; asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory"); return v;
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory"); return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void ats_or(uint32_t a, uint32_t v) { asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
-__device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // LSB-first bit reader of one sub-block. The thread's bitstream is staged through its own 8 x 16-byte ring in
 // shared memory by cp.async (LDGSTS), issued 6-7 chunks (~100 bits x 7) ahead of use, so no global-load latency
@@ -193,8 +212,8 @@ struct BitRing {
     for (uint32_t k = 0; k < 7; ++k) issue(c0 + k);
     cp_wait_n<6>();                                  // chunk c0 landed
     if ((w0 & 3u) == 3u) { issue(c0 + 7); cp_wait_n<6>(); }   // hi lies in chunk c0 + 1
-    lo = ring[w0 & 31u];
-    hi = ring[(w0 + 1) & 31u];
+    lo = lds32(ring_s + ((w0 & 31u) << 2));
+    hi = lds32(ring_s + (((w0 + 1) & 31u) << 2));
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
   __device__ __forceinline__ void consume(uint32_t n) {
@@ -208,7 +227,7 @@ struct BitRing {
         issue((nw >> 2) + 6);
         cp_wait_n<6>();
       }
-      hi = ring[nw & 31u];
+      hi = lds32(ring_s + ((nw & 31u) << 2));
     }
   }
   __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0) * 32 + pos - pos0; }
@@ -327,6 +346,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
+  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);  // last in-file 16-byte chunk offset
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
@@ -368,7 +388,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       while (!err) {
         if (!last && si >= nseq) break;
         const uint32_t pk = in.peek();
-        uint32_t ent = lut_ll[pk & lmask];
+        uint32_t ent = lds32(lut_ll_s + ((pk & lmask) << 2));
         uint32_t len = ent & 15u;
         if (LONG && len == 0) {                         // code longer than the table index (cwl > 11)
           const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
@@ -381,7 +401,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
         const uint32_t L = ((ent >> 8) & 511u) + ((pk >> len) & ((1u << xb) - 1u));
         in.consume(len + xb);
         const uint32_t pd = in.peek();
-        uint32_t de = lut_d[pd & lmask];
+        uint32_t de = lds32(lut_d_s + ((pd & lmask) << 2));
         uint32_t dl = de & 15u;
         if (LONG && isl && dl == 0) {
           const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
@@ -423,10 +443,14 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
 // with coalesced 16-byte stores. Literal bytes are staged into a per-warp shared-memory ring ahead of use
 // with cp.async (LDGSTS) in 512-byte units; records are prefetched four groups ahead in registers. A group too
 // large for the rings (e.g. 32 literal runs of 1023 bytes) is processed directly in global memory.
+// All shared-memory traffic uses 32-bit shared-window addresses (ld/st.shared), never generic pointers.
 constexpr uint32_t kLitRing = 2048;
-constexpr uint32_t kLitUnit = 512;   // 32 lanes x 16 B per cp.async instruction
-constexpr uint32_t kLitAhead = 1024; // prefetch distance in literal bytes
-constexpr uint32_t kPrmBytes = 32 * 16;  // per-warp table of the group's 32 sequence descriptors (DE pass)
+constexpr uint32_t kLitUnit = 512;    // 32 lanes x 16 B per cp.async instruction
+constexpr uint32_t kLitAhead = 1024;  // prefetch distance in literal bytes
+constexpr uint32_t kPrmBytes = 32 * 16;  // the group's 32 sequence descriptors (DE pass)
+
+// per-warp shared layout: [ring RING][literal ring 2 KiB][descriptors 512 B][row-start bitmap RING/8 B]
+__host__ __device__ constexpr uint32_t lz_warp_bytes(uint32_t ring) { return ring + kLitRing + kPrmBytes + ring / 8; }
 
 // byte-granular copy without overlap (dist >= L, reading R2), global memory (slow path)
 __device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_t n) {
@@ -446,30 +470,28 @@ __device__ __forceinline__ void copy_lits_global(uint8_t* d, const uint8_t* __re
   for (; k < n; ++k) d[k] = __ldg(s + k);
 }
 
-// Copy n bytes between power-of-two shared-memory rings (masks dm/sm = size-1), source range not overlapping
-// the destination range: byte head until the destination is word aligned, then aligned 32-bit stores of
-// funnel-shifted source words (bytes of a source word outside [s, s+n) are discarded), byte tail.
-__device__ __forceinline__ void ring_copy(uint8_t* D, uint32_t dm, uint32_t d, const uint8_t* S, uint32_t sm,
-                                          uint32_t s, uint32_t n) {
+// Copy n bytes between power-of-two shared rings (base addresses D/S, masks dm/sm = size-1); the source range
+// does not overlap the destination range: byte head until the destination is word aligned, aligned 32-bit
+// stores of funnel-shifted source words (bytes of a source word outside [s, s+n) are discarded), byte tail.
+__device__ __forceinline__ void ring_copy(uint32_t D, uint32_t dm, uint32_t d, uint32_t S, uint32_t sm, uint32_t s,
+                                          uint32_t n) {
   uint32_t h = (4u - (d & 3u)) & 3u;
   if (h > n) h = n;
-  for (uint32_t k = 0; k < h; ++k) D[(d + k) & dm] = S[(s + k) & sm];
+  for (uint32_t k = 0; k < h; ++k) sts8(D + ((d + k) & dm), lds8(S + ((s + k) & sm)));
   d += h; s += h; n -= h;
   const uint32_t nw = n >> 2;
   if (nw) {
-    const uint32_t* S32 = reinterpret_cast<const uint32_t*>(S);
-    uint32_t* D32 = reinterpret_cast<uint32_t*>(D);
-    const uint32_t swm = sm >> 2, dwm = dm >> 2, sh = (s & 3u) * 8u;
-    uint32_t sw = s >> 2, dw = d >> 2;
-    uint32_t lo = S32[sw & swm];
+    const uint32_t sh = (s & 3u) * 8u;
+    uint32_t sw = s & ~3u;
+    uint32_t lo = lds32(S + (sw & sm));
     for (uint32_t k = 0; k < nw; ++k) {
-      const uint32_t hi = S32[(sw + 1) & swm];
-      D32[dw & dwm] = __funnelshift_r(lo, hi, sh);
-      lo = hi; ++sw; ++dw;
+      const uint32_t hi = lds32(S + ((sw + 4) & sm));
+      sts32(D + (d & dm), __funnelshift_r(lo, hi, sh));
+      lo = hi; sw += 4; d += 4;
     }
-    d += nw * 4; s += nw * 4; n -= nw * 4;
+    s += nw * 4; n -= nw * 4;
   }
-  for (uint32_t k = 0; k < n; ++k) D[(d + k) & dm] = S[(s + k) & sm];
+  for (uint32_t k = 0; k < n; ++k) sts8(D + ((d + k) & dm), lds8(S + ((s + k) & sm)));
 }
 
 struct GlobalOut {
@@ -477,16 +499,14 @@ struct GlobalOut {
   __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { copy_nolap(out + dst, out + src, n); }
 };
 struct RingOut {
-  uint8_t* ring;
-  uint32_t rm;
+  uint32_t ring, rm;
   __device__ __forceinline__ void copy(uint32_t dst, uint32_t src, uint32_t n) const { ring_copy(ring, rm, dst, ring, rm, src, n); }
 };
 
-// a7 for one warp group: back-references of the lanes with has = (L > 0). Returns false on NO_PROGRESS.
+// a7 for one warp group with per-lane copies: MRR (Fig. alg:mrr) or SC. Returns false on NO_PROGRESS.
 template <int STRAT, bool STATS, class Out>
 __device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint32_t lane, bool has, uint32_t dst,
-                                              uint32_t src, uint32_t L, uint32_t op, uint32_t o_carry, uint32_t b,
-                                              uint32_t g0) {
+                                              uint32_t src, uint32_t L, uint32_t op, uint32_t b, uint32_t g0) {
   if (STRAT == GOMP_STRAT_SC) {          // Sequential Copying
     __syncwarp();
     uint32_t m = __ballot_sync(FULL, has);
@@ -498,110 +518,88 @@ __device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint3
     }
     return true;
   }
-  bool use_mrr = STRAT == GOMP_STRAT_MRR;
-  if (STRAT == GOMP_STRAT_DE) {
-    // DE rule (FORMAT.md §4): every source lies below the group start or inside the lane's own literal, so
-    // all lanes copy in one round with no inter-lane ordering
-    const bool de_ok = !has || src + L <= o_carry || src >= op;
-    if (__all_sync(FULL, de_ok)) {
-      if (has) o.copy(dst, src, L);
-      if (STATS) {
-        const uint32_t any = __ballot_sync(FULL, has);
-        uint32_t bytes = has ? L : 0u;
+  // MRR (Fig. alg:mrr): HWM = destination of the lowest pending lane = end of the gap-free written prefix
+  // (R1); a lane is ready when its source lies below HWM or inside its own literal string (R4)
+  __syncwarp();
+  bool pending = has;
+  uint32_t votes = __ballot_sync(FULL, pending);
+  uint32_t rounds = 0;
+  while (votes) {
+    const uint32_t p = __ffs(votes) - 1;
+    const uint32_t hwm = __shfl_sync(FULL, dst, p);
+    const bool ready = pending && (src + L <= hwm || src >= op);
+    if (ready) o.copy(dst, src, L);
+    ++rounds;
+    if (STATS) {
+      uint32_t bytes = ready ? L : 0u;
 #pragma unroll
-        for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
-        if (lane == 0) {
-          atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
-          if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
-        }
-      }
-    } else {
-      use_mrr = true;
-      if (STATS && lane == 0) atomicAdd(stats_ptr(a) + 66, 1ull);
+      for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+      if (lane == 0 && rounds < 33) atomicAdd(stats_ptr(a) + 33 + rounds, (unsigned long long)bytes);
     }
-  }
-  if (use_mrr) {
-    // MRR (Fig. alg:mrr): HWM = destination of the lowest pending lane = end of the gap-free written prefix
-    // (R1); a lane is ready when its source lies below HWM or inside its own literal string (R4)
+    if (!__any_sync(FULL, ready)) {
+      if (lane == 0) report(a, GOMP_ERR_NO_PROGRESS, b, g0);
+      return false;
+    }
+    pending = pending && !ready;
     __syncwarp();
-    bool pending = has;
-    uint32_t votes = __ballot_sync(FULL, pending);
-    uint32_t rounds = 0;
-    while (votes) {
-      const uint32_t p = __ffs(votes) - 1;
-      const uint32_t hwm = __shfl_sync(FULL, dst, p);
-      const bool ready = pending && (src + L <= hwm || src >= op);
-      if (ready) o.copy(dst, src, L);
-      ++rounds;
-      if (STATS) {
-        uint32_t bytes = ready ? L : 0u;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
-        if (lane == 0 && rounds < 33) atomicAdd(stats_ptr(a) + 33 + rounds, (unsigned long long)bytes);
-      }
-      if (!__any_sync(FULL, ready)) {
-        if (lane == 0) report(a, GOMP_ERR_NO_PROGRESS, b, g0);
-        return false;
-      }
-      pending = pending && !ready;
-      __syncwarp();
-      votes = __ballot_sync(FULL, pending);
-    }
-    if (STATS && lane == 0) atomicAdd(stats_ptr(a) + (rounds < 33 ? rounds : 32), 1ull);
+    votes = __ballot_sync(FULL, pending);
   }
+  if (STATS && lane == 0) atomicAdd(stats_ptr(a) + (rounds < 33 ? rounds : 32), 1ull);
   return true;
-}
-
-__device__ __forceinline__ void cp_wait(uint32_t allowed) {
-  if (allowed >= 2) asm volatile("cp.async.wait_group 2;\n" ::);
-  else if (allowed == 1) asm volatile("cp.async.wait_group 1;\n" ::);
-  else asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 // DE group as byte rows (a6 + a7 fused). Group-relative positions x in [0, T) (T = group output bytes).
 // Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte x is lring[x + ld_i], match part
 // [dst_i, opr_{i+1}) whose byte x is (own_i ? lring : ring)[x + md_i] (own_i: source inside its own literal,
 // reading R4). Under the DE rule no source lies in this group's output, so the group is computed in rows of
-// 32 consecutive bytes, lane t owning byte base + t: the owner sequence comes from a one-instruction OR-vote of
-// the row's sequence starts (REDUX) and a popcount; its descriptor is one broadcast 16-byte shared load.
-// Uniform control flow, no divergence, no inter-lane ordering (P:295-329 taken to byte granularity).
-__device__ __forceinline__ void de_group_rows(uint8_t* ring, uint32_t RM, const uint8_t* lring, uint32_t LM,
-                                              uint4* prm, uint32_t lane, bool act, bool has, uint32_t opr,
-                                              uint32_t lit, uint32_t lpos, uint32_t dist, bool own, uint32_t o,
-                                              uint32_t T) {
+// 32 consecutive bytes, lane t owning byte base + t. Row r's sequence starts are word r of a shared bitmap
+// (set with one ATOMS.OR per lane), so the owner of byte x is c0 + popc(bits <= lane) - 1; its descriptor is
+// one broadcast 16-byte shared load. Four rows per step: every load of a step precedes its stores (sources
+// never lie in this group's output). Uniform control flow, no inter-lane ordering (P:295-329 at byte level).
+__device__ __forceinline__ void de_group_rows(uint32_t ring, uint32_t RM, uint32_t lring, uint32_t LM,
+                                              uint32_t prm, uint32_t bits, uint32_t lane, bool act, bool has,
+                                              uint32_t opr, uint32_t lit, uint32_t lpos, uint32_t dist, bool own,
+                                              uint32_t o, uint32_t T) {
   const uint32_t dstr = opr + lit;
   const uint32_t ld = lpos - opr;                                  // lring position of byte x = x + ld
-  const uint32_t md = (has && own) ? ld - dist : o - dist;         // match source position = x + md
-  prm[lane] = make_uint4(opr, dstr | ((has && own) ? 0x80000000u : 0u), ld, md);
+  const bool own_ = has && own;
+  const uint32_t md = own_ ? ld - dist : o - dist;                 // match source position = x + md
+  sts128(prm + lane * 16, make_uint4(opr, dstr | (own_ ? 0x80000000u : 0u), ld, md));
+  if (act) ats_or(bits + (opr >> 5) * 4, 1u << (opr & 31));
   __syncwarp();
   const uint32_t le = (2u << lane) - 1u;                           // lanes <= this lane
   uint32_t c0 = 0;                                                 // sequences starting before the row
-  // four rows per step: all loads of a step issue before its stores (sources never lie in this group's
-  // output, so the stores cannot alias them) to keep the shared-memory latency off the serial chain
   for (uint32_t base0 = 0; base0 < T; base0 += 128) {
+    const uint4 Mv = lds128(bits + (base0 >> 5) * 4);
+    const uint32_t Ms[4] = {Mv.x, Mv.y, Mv.z, Mv.w};
     uint32_t byte[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint32_t base = base0 + 32 * r;
-      const uint32_t rel = opr - base;
-      const uint32_t M = __reduce_or_sync(FULL, (act && rel < 32u) ? (1u << rel) : 0u);
-      const uint32_t j = c0 + __popc(M & le) - 1u;
-      c0 += __popc(M);
-      const uint32_t x = base + lane;
+      const uint32_t x = base0 + 32 * r + lane;
+      const uint32_t j = c0 + __popc(Ms[r] & le) - 1u;
+      c0 += __popc(Ms[r]);
       byte[r] = 0;
       if (x < T) {
-        const uint4 D = prm[j];
+        const uint4 D = lds128(prm + j * 16);
         const bool in_lit = x < (D.y & 0x7fffffffu);
         const uint32_t p = x + (in_lit ? D.z : D.w);
-        byte[r] = (in_lit || (D.y >> 31)) ? lring[p & LM] : ring[p & RM];
+        byte[r] = (in_lit || (D.y >> 31)) ? lds8(lring + (p & LM)) : lds8(ring + (p & RM));
       }
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint32_t x = base0 + 32 * r + lane;
-      if (x < T) ring[(o + x) & RM] = uint8_t(byte[r]);
+      if (x < T) sts8(ring + ((o + x) & RM), byte[r]);
     }
   }
+  // clear the bitmap words this group used (the group-end __syncwarp orders this before the next group)
+  for (uint32_t wd = lane; wd < (T + 31) / 32; wd += 32) sts32(bits + wd * 4, 0u);
+}
+
+__device__ __forceinline__ void cp_wait(uint32_t allowed) {
+  if (allowed >= 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+  else if (allowed == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 template <int STRAT, bool STATS>
@@ -611,9 +609,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wi >= a.n_blocks) return;
   const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLitRing - 1;
-  uint8_t* ring = lz_smem + (threadIdx.x >> 5) * (RING + kLitRing + kPrmBytes);
-  uint8_t* lring = ring + RING;
-  uint4* prm = reinterpret_cast<uint4*>(lring + kLitRing);
+  const uint32_t ring = uint32_t(__cvta_generic_to_shared(lz_smem)) + (threadIdx.x >> 5) * lz_warp_bytes(RING);
+  const uint32_t lring = ring + RING, prm = lring + kLitRing, bits = prm + kPrmBytes;
+  for (uint32_t wd = lane; wd < RING / 32; wd += 32) sts32(bits + wd * 4, 0u);
   const uint32_t b = a.first_block + wi;
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
@@ -636,7 +634,6 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const uint8_t* lal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits) & ~uintptr_t(15));
   const uint32_t lofs = uint32_t(lits - lal);
   const uint32_t lend16 = (lofs + e.n_lit + 15u) & ~15u;
-  const uint32_t lring_s = uint32_t(__cvta_generic_to_shared(lring));
   uint32_t lf = 0;  // literal bytes (rel) issued to the ring, multiple of kLitUnit
   uint8_t* out = a.dst + uint64_t(wi) * a.block_size;
   const uint32_t mm1 = a.min_match - 1, n_seq = e.n_seq;
@@ -681,7 +678,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       const uint32_t need = lofs + l_carry + lit_sum;
       while (lf < need + kLitAhead && lf < lend16 && lf + kLitUnit <= lofs + l_carry + kLitRing) {
         const uint32_t off = lf + lane * 16;
-        if (off < lend16) cp_async16(lring_s + (off & LM), lal + off);
+        if (off < lend16) cp_async16(lring + (off & LM), lal + off);
         cp_commit();
         lf += kLitUnit;
       }
@@ -696,7 +693,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
         // group's output rows, balanced over the lanes, with no inter-lane ordering at all.
         const bool de_ok = !has || src + L <= o_carry || src >= op;
         if (__all_sync(FULL, de_ok)) {
-          de_group_rows(ring, RM, lring, LM, prm, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
+          de_group_rows(ring, RM, lring, LM, prm, bits, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
                         o_carry, out_sum);
           if (STATS) {
             const uint32_t any = __ballot_sync(FULL, has);
@@ -717,26 +714,28 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
         // a6: literal strings into the output ring; a7: back-references inside the ring (MRR / SC)
         if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
         constexpr int S2 = STRAT == GOMP_STRAT_DE ? GOMP_STRAT_MRR : STRAT;
-        if (!resolve_group<S2, STATS>(a, ro, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+        if (!resolve_group<S2, STATS>(a, ro, lane, has, dst, src, L, op, b, g0)) return;
       }
       __syncwarp();
       // flush completed 16-byte chunks to HBM (coalesced 16-byte stores)
       const uint32_t q1 = (o_carry + out_sum) >> 4;
       for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
-        reinterpret_cast<uint4*>(out)[q] = reinterpret_cast<const uint4*>(ring)[q & (RM >> 4)];
+        reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
       if (q1 * 16 > flushed) flushed = q1 * 16;
     } else {
       // group too large for the rings: flush the ring, run the group in global memory, reload the window
       __syncwarp();
-      for (uint32_t p = flushed + lane; p < o_carry; p += 32) out[p] = ring[p & RM];
+      for (uint32_t p = flushed + lane; p < o_carry; p += 32) out[p] = uint8_t(lds8(ring + (p & RM)));
       flushed = o_carry;
       __syncwarp();
       if (act) copy_lits_global(out + op, lits + lp, lit);
-      if (!resolve_group<STRAT, STATS>(a, go, lane, has, dst, src, L, op, o_carry, b, g0)) return;
+      if (!resolve_group<STRAT == GOMP_STRAT_SC ? GOMP_STRAT_SC : GOMP_STRAT_MRR, STATS>(a, go, lane, has, dst, src,
+                                                                                       L, op, b, g0))
+        return;
       __syncwarp();
       const uint32_t o_new = o_carry + out_sum;
       const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
-      for (uint32_t p = o_new - keep + lane; p < o_new; p += 32) ring[p & RM] = out[p];
+      for (uint32_t p = o_new - keep + lane; p < o_new; p += 32) sts8(ring + (p & RM), out[p]);
       flushed = o_new;
       cp_wait(0);
       lf = ((lofs + l_carry + lit_sum) / kLitUnit) * kLitUnit;
@@ -753,11 +752,11 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   }
   const uint32_t q1 = o_carry >> 4;
   for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
-    reinterpret_cast<uint4*>(out)[q] = reinterpret_cast<const uint4*>(ring)[q & (RM >> 4)];
-  for (uint32_t p = max(q1 * 16, flushed) + lane; p < o_carry; p += 32) out[p] = ring[p & RM];
+    reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
+  for (uint32_t p = max(q1 * 16, flushed) + lane; p < o_carry; p += 32) out[p] = uint8_t(lds8(ring + (p & RM)));
 }
 
-size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * (ring + kLitRing + kPrmBytes); }
+size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * lz_warp_bytes(ring); }
 
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
