@@ -1,6 +1,6 @@
 // decode.cu — sm_100a kernels of the Gompresso decompression hot path and their C-ABI launchers.
 //
-//   huff_decode_kernel  Gompresso/Bit, one CTA per data block:
+//   huff_thread_kernel / huff_warp_kernel  Gompresso/Bit, one CTA per data block:
 //       a1 block-table entry checks; a2 CTA-wide exclusive scans of the sub-block bit sizes and literal counts
 //       (P:48-50); a3 canonical code lengths -> two 2^LB-entry lookup tables in shared memory
 //       (P:73-77); a4 one thread per sub-block decodes its bitstream with one table lookup per
@@ -119,15 +119,15 @@ struct HuffSmem {
   uint16_t sorted_d[32];
   uint8_t lens[320];     // 286 litlen + 30 dist code lengths
   uint32_t bad;
-  uint32_t wlits[8];
-  uint64_t wbits[8];
+  uint32_t wlits[16];
+  uint64_t wbits[16];
   uint64_t carry_bits;
   uint32_t carry_lits;
 };
 
 // canonical walk for codes longer than the table index (cwl > lut_bits): bits are taken LSB-first from buf
 // returns symbol | length << 16, or -1 if no code matches
-__device__ int canon_slow(uint64_t buf, const CanonTab& t, const uint16_t* sorted) {
+__device__ int canon_slow(uint32_t buf, const CanonTab& t, const uint16_t* sorted) {
   int code = 0, first = 0, index = 0;
   for (int l = 1; l <= 15; ++l) {
     code |= int((buf >> (l - 1)) & 1u);
@@ -184,36 +184,36 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// LSB-first bit reader of one sub-block. The thread's bitstream is staged through its own 8 x 16-byte ring in
-// shared memory by cp.async (LDGSTS), issued 6-7 chunks (~100 bits x 7) ahead of use, so no global-load latency
-// sits on the per-symbol dependency chain. The current 64-bit window is two registers (lo, hi) and a bit
+// LSB-first bit reader of one bitstream segment. The stream is staged through the thread's own ring of NC
+// 16-byte chunks in shared memory by cp.async (LDGSTS), issued NC-1 chunks ahead of use, so no global-load
+// latency sits on the per-symbol dependency chain. The 64-bit window is two registers (lo, hi) and a bit
 // offset: peek() = one funnel shift; consume(n <= 32) crosses at most one word, which costs one shared load.
 // Chunk addresses are clamped to the file (bytes past the stream are never used).
+template <uint32_t NC>
 struct BitRing {
-  const uint32_t* ring;  // this thread's 32-word ring (shared memory)
-  uint32_t ring_s;       // its shared-window address for cp.async
-  const uint8_t* gbase;  // 16-aligned start of the block's bitstream
-  uint64_t gmax;         // last valid 16-byte chunk offset from gbase
-  uint32_t w, w0, lo, hi, pos, pos0, c0;
+  static constexpr uint32_t WM = NC * 4 - 1;   // word mask of the ring
+  uint32_t ring;                               // shared-window address of this thread's ring
+  const uint8_t* gbase;                        // 16-aligned start of the block's bitstream
+  uint64_t gmax;                               // last valid 16-byte chunk offset from gbase
+  uint32_t w, w0, lo, hi, pos, pos0;
   __device__ __forceinline__ void issue(uint32_t c) {
     const uint64_t off = uint64_t(c) * 16u;
-    cp_async16(ring_s + (c & 7u) * 16u, gbase + (off <= gmax ? off : gmax));
+    cp_async16(ring + (c % NC) * 16u, gbase + (off <= gmax ? off : gmax));
     cp_commit();
   }
-  __device__ __forceinline__ void init(const uint32_t* r, const uint8_t* gb, uint64_t gm, uint64_t start) {
+  __device__ __forceinline__ void init(uint32_t r, const uint8_t* gb, uint64_t gm, uint32_t start) {
     ring = r;
-    ring_s = uint32_t(__cvta_generic_to_shared(r));
     gbase = gb;
     gmax = gm;
-    w0 = w = uint32_t(start >> 5);
-    pos0 = pos = uint32_t(start & 31);
-    c0 = w0 >> 2;
+    w0 = w = start >> 5;
+    pos0 = pos = start & 31;
+    const uint32_t c0 = w0 >> 2;
 #pragma unroll
-    for (uint32_t k = 0; k < 7; ++k) issue(c0 + k);
-    cp_wait_n<6>();                                  // chunk c0 landed
-    if ((w0 & 3u) == 3u) { issue(c0 + 7); cp_wait_n<6>(); }   // hi lies in chunk c0 + 1
-    lo = lds32(ring_s + ((w0 & 31u) << 2));
-    hi = lds32(ring_s + (((w0 + 1) & 31u) << 2));
+    for (uint32_t k = 0; k + 1 < NC; ++k) issue(c0 + k);
+    cp_wait_n<NC - 2>();                                       // chunk c0 landed
+    if ((w0 & 3u) == 3u) { issue(c0 + NC - 1); cp_wait_n<NC - 2>(); }   // hi lies in chunk c0 + 1
+    lo = lds32(ring + ((w0 & WM) << 2));
+    hi = lds32(ring + (((w0 + 1) & WM) << 2));
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
   __device__ __forceinline__ void consume(uint32_t n) {
@@ -223,54 +223,72 @@ struct BitRing {
       ++w;
       lo = hi;
       const uint32_t nw = w + 1;
-      if ((nw & 3u) == 0) {                          // entering chunk nw/4: top up the ring, wait for it
-        issue((nw >> 2) + 6);
-        cp_wait_n<6>();
+      if ((nw & 3u) == 0) {                                    // entering chunk nw/4: top up, wait for it
+        issue((nw >> 2) + NC - 2);
+        cp_wait_n<NC - 2>();
       }
-      hi = lds32(ring_s + ((nw & 31u) << 2));
+      hi = lds32(ring + ((nw & WM) << 2));
     }
   }
-  __device__ __forceinline__ uint64_t consumed() const { return uint64_t(w - w0) * 32 + pos - pos0; }
+  __device__ __forceinline__ uint32_t at() const { return w * 32 + pos; }  // absolute bit position
+  __device__ __forceinline__ void drain() const { cp_wait_n<0>(); }
 };
 
-// ------------------------------------------------------------------ K1: sub-block Huffman decode (Bit)
-template <bool LONG>   // LONG: cwl > lut_bits, codes longer than the table index take the canonical walk
-__global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
-  uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
-  const uint32_t lut_n = 1u << a.lut_bits;
-  uint32_t* lut_d = lut_ll + lut_n;
-  uint32_t* bit_rings = lut_d + lut_n;                  // 32 words per thread
-
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
-  const BlockEntry e = load_entry(a.src, b, lane);
-  const uint32_t ulen = block_ulen(a, b);
-
-  // a1: table checks (uniform across the CTA)
-  bool ok = payload_ok(a, e) && e.payload_len >= kTreeBytes && e.S >= 1 &&
-            e.n_sub == (e.n_seq + e.S - 1) / e.S && uint64_t(e.sub_first) + e.n_sub <= a.n_sub_total &&
-            4ull * e.n_seq + e.n_lit <= a.max_tok && e.n_lit <= ulen && e.n_seq <= ulen;
-  if (!ok) {
-    if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
-    return;
+// One decode iteration (one table lookup per symbol): a litlen symbol and, for a length code, its
+// extra bits, the distance symbol and its extra bits. kind: K_LIT / K_LEN / K_EOB / K_BAD.
+struct Step {
+  uint32_t kind, L, dist, byte, bad;
+};
+template <bool LONG, class BR>
+__device__ __forceinline__ Step decode_step(BR& in, uint32_t lut_ll_s, uint32_t lut_d_s, uint32_t lmask,
+                                            const HuffSmem& sm) {
+  Step st;
+  const uint32_t pk = in.peek();
+  uint32_t ent = lds32(lut_ll_s + ((pk & lmask) << 2));
+  uint32_t len = ent & 15u;
+  if (LONG && len == 0) {                                      // code longer than the table index
+    const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
+    ent = sl < 0 ? (K_BAD << 4) | 1u : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
+    len = ent & 15u;
   }
-  const uint8_t* pl = a.src + e.payload_off;
+  st.kind = (ent >> 4) & 3u;
+  const bool isl = st.kind == K_LEN;
+  const uint32_t xb = isl ? (ent >> 17) & 7u : 0u;
+  st.L = ((ent >> 8) & 511u) + ((pk >> len) & ((1u << xb) - 1u));
+  st.byte = (ent >> 8) & 255u;
+  in.consume(len + xb);
+  const uint32_t pd = in.peek();
+  uint32_t de = lds32(lut_d_s + ((pd & lmask) << 2));
+  uint32_t dl = de & 15u;
+  if (LONG && isl && dl == 0) {
+    const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
+    de = sl < 0 ? (K_BAD << 4) | 1u : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
+    dl = de & 15u;
+  }
+  const uint32_t dx = (de >> 24) & 15u;
+  st.dist = ((de >> 8) & 0xffffu) + ((pd >> dl) & ((1u << dx) - 1u));
+  in.consume(isl ? dl + dx : 0u);
+  st.bad = isl && ((de >> 4) & 3u) == K_BAD;
+  return st;
+}
+
+// a1 + a3 for one data block, whole CTA: unpack the nibble code lengths, canonical tables (warp 0; counts,
+// first codes, sorted symbols by __match_any_sync ranks) and the entry-parallel fill of both LUTs in shared
+// memory. Unresolved entries: 0 (LONG: canonical walk) or K_BAD. Returns false (uniformly) on a bad tree.
+template <bool LONG>
+__device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, const uint8_t* pl, const Args& a) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lut_n = 1u << a.lut_bits;
   if (tid == 0) { sm.bad = 0; sm.carry_bits = 0; sm.carry_lits = 0; }
-  if (tid < 32) {
-    for (int t = 0; t < 2; ++t) {
-      if (lane < 16) { sm.tab[t].count[lane] = 0; sm.tab[t].running[lane] = 0; }
-    }
+  if (tid < 16) {
+    sm.tab[0].count[tid] = 0; sm.tab[0].running[tid] = 0;
+    sm.tab[1].count[tid] = 0; sm.tab[1].running[tid] = 0;
   }
-  // unpack the 286 + 30 nibble code lengths (FORMAT.md §3)
   for (uint32_t s = tid; s < 316; s += blockDim.x) {
     const uint32_t byte = s < 286 ? pl[s >> 1] : pl[143 + ((s - 286) >> 1)];
     const uint32_t nib = s < 286 ? (s & 1) : ((s - 286) & 1);
     sm.lens[s] = uint8_t((byte >> (4 * nib)) & 15u);
   }
   __syncthreads();
-  // a3: canonical tables, warp 0 (count / first / index / sorted symbols via __match_any_sync ranks)
   if (warp == 0) {
     uint32_t badl = 0;
     for (int t = 0; t < 2; ++t) {
@@ -315,11 +333,7 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
     if (lane == 0 && badl) sm.bad = 1;
   }
   __syncthreads();
-  if (sm.bad) {
-    if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
-    return;
-  }
-  // a3: fill both LUTs entry-parallel: index i holds the next lut_bits stream bits (LSB-first)
+  if (sm.bad) return false;
   const uint32_t LB = a.lut_bits;
   for (uint32_t i = tid; i < 2 * lut_n; i += blockDim.x) {
     const int t = i >= lut_n;
@@ -338,16 +352,77 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
     (t ? lut_d : lut_ll)[idx] = ent;
   }
   __syncthreads();
+  return true;
+}
 
-  // a2 + a4: sub-blocks in chunks of blockDim; CTA-wide exclusive scans give start bit and literal offset
+__device__ __forceinline__ bool huff_block_ok(const Args& a, const BlockEntry& e, uint32_t ulen) {
+  return payload_ok(a, e) && e.payload_len >= kTreeBytes && e.S >= 1 && e.n_sub == (e.n_seq + e.S - 1) / e.S &&
+         uint64_t(e.sub_first) + e.n_sub <= a.n_sub_total && 4ull * e.n_seq + e.n_lit <= a.max_tok &&
+         e.n_lit <= ulen && e.n_seq <= ulen;
+}
+
+// Serial decode of one whole sub-block by one thread (the paper's thread-per-sub-block scheme):
+// records at rec[0..nseq), literals at lit[0..nl). Returns 0 or a CorruptStream detail code.
+template <bool LONG, class BR>
+__device__ uint32_t decode_sub_serial(BR& in, uint32_t lut_ll_s, uint32_t lut_d_s, uint32_t lmask, const HuffSmem& sm,
+                                      const Args& a, uint32_t* rec, uint8_t* lit, uint32_t nseq, uint32_t nl,
+                                      bool last, uint32_t bsz) {
+  const uint32_t mm1 = a.min_match - 1, b0 = in.at();
+  uint32_t si = 0, lw = 0, run = 0, bad = 0, kind = K_LIT;
+  for (;;) {
+    if (!last && si >= nseq) break;
+    const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+    kind = st.kind;
+    const bool isl = kind == K_LEN, islit = kind == K_LIT;
+    if (islit && lw < nl) lit[lw] = uint8_t(st.byte);
+    lw += islit ? 1u : 0u;
+    run += islit ? 1u : 0u;
+    // R10/R16: a sequence closes at a length code, at 1023 literals, or at EOB with pending literals
+    const bool close = isl || (islit && run == kMaxLitRun) || (kind == K_EOB && run != 0);
+    if (close && si < nseq) rec[si] = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
+    si += close ? 1u : 0u;
+    run = close ? 0u : run;
+    bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match));
+    if (kind >= K_EOB || lw > nl || si > nseq || in.at() - b0 > bsz) break;
+  }
+  if (bad) return 6;
+  if (kind == K_BAD) return 2;
+  if (kind == K_EOB && !last) return 7;
+  if (si != nseq || run != 0 || lw != nl || in.at() - b0 != bsz) return 9;
+  return 0;
+}
+
+// ------------------------------------------------------------------ K1a: thread-per-sub-block decode (Bit)
+// One CTA per data block; thread k decodes sub-blocks k, k+blockDim, ... (used when sub-blocks are small,
+// e.g. the paper's 16-sequence sub-blocks, where there are thousands per block).
+template <bool LONG>
+__global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
+  uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
+  const uint32_t lut_n = 1u << a.lut_bits;
+  uint32_t* lut_d = lut_ll + lut_n;
+  const uint32_t rings_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n));   // 128 B per thread
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
+  const BlockEntry e = load_entry(a.src, b, lane);
+  if (!huff_block_ok(a, e, block_ulen(a, b))) {
+    if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
+    return;
+  }
+  const uint8_t* pl = a.src + e.payload_off;
+  if (!build_tables<LONG>(sm, lut_ll, lut_d, pl, a)) {
+    if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+    return;
+  }
+  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint8_t* subt = a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total;
   uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
-  const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
-  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
-  const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);  // last in-file 16-byte chunk offset
+  const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
+  // a2: CTA-wide exclusive scans of the sub-block bit sizes and literal counts, chunk by chunk
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
     uint32_t bsz = 0, nl = 0;
@@ -375,65 +450,263 @@ __global__ void __launch_bounds__(256) huff_decode_kernel(const Args a) {
       if (start + bsz > bit_limit || uint64_t(lstart) + nl > e.n_lit) err = 1;
       const uint32_t seq0 = k * e.S;
       const uint32_t nseq = (k + 1 == e.n_sub) ? e.n_seq - seq0 : e.S;
-      const bool last = k + 1 == e.n_sub;
-      uint32_t* rec = rec_base + seq0;
-      uint8_t* lit = lit_base + lstart;
-      uint32_t si = 0, lw = 0, run = 0;
-      BitRing in;
-      in.init(bit_rings + 32 * tid, pl + kTreeBytes, gmax, err ? 0 : start);
-      // one litlen symbol per iteration; a length symbol also takes its distance in the same iteration.
-      // The body is branch-light (predicated stores, deferred checks) so the lanes (sub-blocks) of a warp stay
-      // converged (one table lookup per symbol).
-      uint32_t kind = K_LIT, bad = 0;
-      while (!err) {
-        if (!last && si >= nseq) break;
-        const uint32_t pk = in.peek();
-        uint32_t ent = lds32(lut_ll_s + ((pk & lmask) << 2));
-        uint32_t len = ent & 15u;
-        if (LONG && len == 0) {                         // code longer than the table index (cwl > 11)
-          const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
-          ent = sl < 0 ? (K_BAD << 4) | 1u : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-          len = ent & 15u;
-        }
-        kind = (ent >> 4) & 3u;
-        const bool isl = kind == K_LEN, islit = kind == K_LIT;
-        const uint32_t xb = isl ? (ent >> 17) & 7u : 0u;
-        const uint32_t L = ((ent >> 8) & 511u) + ((pk >> len) & ((1u << xb) - 1u));
-        in.consume(len + xb);
-        const uint32_t pd = in.peek();
-        uint32_t de = lds32(lut_d_s + ((pd & lmask) << 2));
-        uint32_t dl = de & 15u;
-        if (LONG && isl && dl == 0) {
-          const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
-          de = sl < 0 ? (K_BAD << 4) : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-          dl = de & 15u;
-        }
-        const uint32_t dx = (de >> 24) & 15u;
-        const uint32_t dist = ((de >> 8) & 0xffffu) + ((pd >> dl) & ((1u << dx) - 1u));
-        in.consume(isl ? dl + dx : 0u);
-        if (islit && lw < nl) lit[lw] = uint8_t(ent >> 8);
-        lw += islit ? 1u : 0u;
-        run += islit ? 1u : 0u;
-        // R10/R16: a sequence closes at a length code, at 1023 literals, or at EOB with pending literals
-        const bool close = isl || (islit && run == kMaxLitRun) || (kind == K_EOB && run != 0);
-        if (close && si < nseq) rec[si] = isl ? (run | ((L - mm1) << 10) | ((dist - 1) << 16)) : run;
-        si += close ? 1u : 0u;
-        run = close ? 0u : run;
-        bad |= isl && (L < a.min_match || L > a.max_match || ((de >> 4) & 3u) == K_BAD || dl == 0);
-        if (kind >= K_EOB || lw > nl || si > nseq) break;
-      }
       if (!err) {
-        if (bad) err = 6;
-        else if (kind == K_BAD) err = 2;
-        else if (kind == K_EOB && !last) err = 7;
-        else if (si != nseq || run != 0 || lw != nl || in.consumed() != bsz) err = 9;
+        BitRing<8> in;
+        in.init(rings_s + tid * 128, pl + kTreeBytes, gmax, uint32_t(start));
+        err = decode_sub_serial<LONG>(in, lut_ll_s, lut_d_s, lut_n - 1, sm, a, rec_base + seq0, lit_base + lstart,
+                                      nseq, nl, k + 1 == e.n_sub, bsz);
+        in.drain();
       }
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
-    cp_wait_n<0>();
   }
   __syncthreads();
   if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
+}
+
+// ------------------------------------------------------------------ K1b: warp-per-sub-block speculative decode
+// B200 answer to "few, long sub-blocks" (BASELINE C2: 16 sub-blocks of ~6 KB per 256 KiB block gives only 16
+// serial chains per block). One warp decodes one sub-block with its 32 lanes: lane p starts at bit p*c of the
+// sub-block (c = ceil(bits/32)), i.e. usually inside a codeword, and decodes speculatively to the first symbol
+// boundary at or after its chunk end, recording its first kRec iteration boundaries. Canonical prefix codes
+// self-synchronise: lane p's path joins the true path when the true exit position of lane p-1 is one of its
+// recorded boundaries; otherwise that lane re-decodes from the true position (a rare serial fix-up). Then warp
+// scans give every lane its record and literal offsets and pass 2 decodes again from the true starts, writing
+// records and literals. Sequences close only at length codes here (a literal run reaching 1023 bytes, R10,
+// makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
+constexpr uint32_t kRec = 12;            // recorded iteration boundaries per lane (self-sync window)
+constexpr uint32_t kSpecRing = 4;        // 16-byte chunks per lane bit ring
+constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this use one lane (serial)
+
+__host__ __device__ constexpr uint32_t spec_warp_bytes() { return 32 * (kSpecRing * 16 + kRec * 8); }
+
+template <bool LONG>
+__global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
+  uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
+  const uint32_t lut_n = 1u << a.lut_bits;
+  uint32_t* lut_d = lut_ll + lut_n;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t wbase_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + warp * spec_warp_bytes();
+  const uint32_t ring_s = wbase_s + lane * (kSpecRing * 16);           // this lane's bit ring
+  const uint32_t recp_s = wbase_s + 32 * kSpecRing * 16;               // [kRec][32] boundary positions
+  const uint32_t recc_s = recp_s + kRec * 32 * 4;                      // [kRec][32] lits | nlen << 16 before it
+  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
+  const BlockEntry e = load_entry(a.src, b, lane);
+  if (!huff_block_ok(a, e, block_ulen(a, b))) {
+    if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
+    return;
+  }
+  const uint8_t* pl = a.src + e.payload_off;
+  if (!build_tables<LONG>(sm, lut_ll, lut_d, pl, a)) {
+    if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+    return;
+  }
+  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
+  const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
+  const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
+  const uint32_t* subt = reinterpret_cast<const uint32_t*>(a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total) +
+                         2ull * e.sub_first;
+  uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
+  uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
+  uint8_t* lit_base = tok + 4ull * e.n_seq;
+  const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
+  const uint8_t* gbits = pl + kTreeBytes;
+  const uint32_t le = (2u << lane) - 1u, lt = (1u << lane) - 1u;
+
+  for (uint32_t k = warp; k < e.n_sub; k += nwarps) {
+    // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
+    uint64_t sb = 0;
+    uint32_t sl = 0;
+    for (uint32_t j = lane; j < k; j += 32) { sb += __ldg(subt + 2 * j); sl += __ldg(subt + 2 * j + 1); }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) { sb += __shfl_xor_sync(FULL, sb, d); sl += __shfl_xor_sync(FULL, sl, d); }
+    const uint32_t bsz = __ldg(subt + 2 * k), nl = __ldg(subt + 2 * k + 1);
+    const uint32_t seq0 = k * e.S;
+    const bool last = k + 1 == e.n_sub;
+    const uint32_t nseq = last ? e.n_seq - seq0 : e.S;
+    uint32_t* rec = rec_base + seq0;
+    uint8_t* lit = lit_base + sl;
+    if (sb + bsz > bit_limit || uint64_t(sl) + nl > e.n_lit) {
+      if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 1u);
+      continue;
+    }
+    const uint32_t S0 = uint32_t(sb);        // absolute start bit of the sub-block in the block's bitstream
+    bool serial = bsz < kSpecMinBits;
+    uint32_t t_start = 0, e_pos = 0, lits_t = 0, nlen_t = 0, lead_t = 0, trail_t = 0, maxrun = 0;
+    bool has_t = false;
+    if (!serial) {
+      // ---------------- pass 1: speculative scan of this lane's chunk
+      const uint32_t c = (bsz + 31) / 32;
+      const uint32_t sp = S0 + lane * c;
+      const uint32_t lim = S0 + min((lane + 1) * c, bsz);
+      uint32_t lits = 0, nlen = 0, lead = 0, trail = 0, first_len_seen = 0, run = 0, it = 0;
+      uint32_t lead_after_rec = 0xffffffffu;     // literals before the first length code after the recorded range
+      BitRing<kSpecRing> in;
+      in.init(ring_s, gbits, gmax, sp);
+      while (in.at() < lim) {
+        const uint32_t pos = in.at();
+        if (it < kRec) {
+          sts32(recp_s + (it * 32 + lane) * 4, pos - S0);
+          sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
+        }
+        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+        if (st.kind == K_BAD) in.consume(1);    // garbage before self-synchronisation (validated in pass 2)
+        const bool isl = st.kind == K_LEN;
+        if (st.kind == K_LIT) { ++lits; ++run; }
+        if (isl) {
+          if (!first_len_seen) lead = lits;
+          if (it + 1 >= kRec && lead_after_rec == 0xffffffffu) lead_after_rec = lits;
+          first_len_seen = 1;
+          ++nlen;
+          maxrun = max(maxrun, run);
+          run = 0;
+        }
+        ++it;
+      }
+      trail = run;
+      if (!first_len_seen) lead = lits;
+      e_pos = in.at() - S0;
+      in.drain();
+      __syncwarp();
+      // ---------------- synchronisation: the true start of lane p is the true exit of lane p-1
+      uint32_t merged = lane == 0 ? 0u : 0xffffffffu;     // recorded index where the true path joins
+      bool fixed = lane == 0;                             // path known to start on the true path
+      for (uint32_t round = 0; round < 33; ++round) {
+        const uint32_t prev_e = __shfl_up_sync(FULL, e_pos, 1);
+        if (!fixed) {
+          merged = 0xffffffffu;
+          const uint32_t rr = min(it, kRec);
+          for (uint32_t r = 0; r < rr; ++r)
+            if (lds32(recp_s + (r * 32 + lane) * 4) == prev_e) { merged = r; break; }
+        }
+        // lane p is on the true path iff every lane before it is: fix the first lane that is not
+        const uint32_t unsynced = __ballot_sync(FULL, merged == 0xffffffffu);
+        if (!unsynced) break;
+        const uint32_t p = __ffs(unsynced) - 1;
+        const uint32_t tstart = __shfl_sync(FULL, e_pos, p - 1);   // true: lanes < p are synced
+        if (lane == p) {
+          const uint32_t lim2 = S0 + min((lane + 1) * c, bsz);
+          lits = 0; nlen = 0; lead = 0; run = 0; first_len_seen = 0; it = 0; lead_after_rec = 0xffffffffu;
+          BitRing<kSpecRing> in2;
+          in2.init(ring_s, gbits, gmax, S0 + tstart);
+          while (in2.at() < lim2) {
+            const uint32_t pos = in2.at();
+            if (it < kRec) {
+              sts32(recp_s + (it * 32 + lane) * 4, pos - S0);
+              sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
+            }
+            const Step st = decode_step<LONG>(in2, lut_ll_s, lut_d_s, lmask, sm);
+            if (st.kind == K_BAD) in2.consume(1);
+            const bool isl = st.kind == K_LEN;
+            if (st.kind == K_LIT) { ++lits; ++run; }
+            if (isl) {
+              if (!first_len_seen) lead = lits;
+              if (it + 1 >= kRec && lead_after_rec == 0xffffffffu) lead_after_rec = lits;
+              first_len_seen = 1;
+              ++nlen;
+              maxrun = max(maxrun, run);
+              run = 0;
+            }
+            ++it;
+          }
+          trail = run;
+          if (!first_len_seen) lead = lits;
+          e_pos = in2.at() - S0;
+          in2.drain();
+          merged = 0;
+          fixed = true;
+        }
+        __syncwarp();
+      }
+      // statistics of the true path = speculative totals minus the prefix before the merge point
+      const uint32_t my_start = lds32(recp_s + (merged * 32 + lane) * 4);
+      const uint32_t cum = lds32(recc_s + (merged * 32 + lane) * 4);
+      const uint32_t lits0 = cum & 0xffffu, nlen0 = cum >> 16;
+      lits_t = lits - lits0;
+      nlen_t = nlen - nlen0;
+      has_t = nlen_t > 0;
+      trail_t = has_t ? trail : lits_t;
+      // literals from the merge point to the first length code after it
+      lead_t = lits_t;
+      if (has_t) {
+        if (nlen0 == 0 && first_len_seen) lead_t = lead - lits0;        // first length code overall is after it
+        else {
+          uint32_t found = 0xffffffffu;
+          const uint32_t rr = min(it, kRec);
+          for (uint32_t r = merged + 1; r < rr; ++r) {
+            const uint32_t cr = lds32(recc_s + (r * 32 + lane) * 4);
+            if ((cr >> 16) > nlen0) { found = r; break; }              // a length code ended before boundary r
+          }
+          // the length code is iteration found-1: literals before it = lits counted at boundary found-1
+          if (found != 0xffffffffu) lead_t = (lds32(recc_s + ((found - 1) * 32 + lane) * 4) & 0xffffu) - lits0;
+          else lead_t = (lead_after_rec != 0xffffffffu ? lead_after_rec : lits) - lits0;
+        }
+      }
+      t_start = my_start;
+      // a literal run of >= 1023 anywhere (R10 closes sequences there): serial fallback for this sub-block
+      uint32_t runin = 0;   // run length entering this lane = carried across lanes without length codes
+      {
+        uint32_t hv = has_t ? 1u : 0u, val = has_t ? trail_t : lits_t;
+        // inclusive scan of (has, val): (h2,v2)∘(h1,v1) = h2 ? (1,v2) : (h1, v1 + v2)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t h1 = __shfl_up_sync(FULL, hv, d), v1 = __shfl_up_sync(FULL, val, d);
+          if (lane >= uint32_t(d) && !hv) { hv = h1; val = v1 + val; }
+        }
+        const uint32_t vprev = __shfl_up_sync(FULL, val, 1);
+        runin = lane == 0 ? 0u : vprev;
+      }
+      const bool longrun = maxrun >= kMaxLitRun || trail_t >= kMaxLitRun || runin + lead_t >= kMaxLitRun;
+      serial = __any_sync(FULL, longrun);
+      if (!serial) {
+        // ---------------- offsets: exclusive scans of sequences (closed by length codes) and literals
+        uint32_t seqs = nlen_t;   // + the EOB-closed final literal-only sequence of the block
+        if (last && lane == 31 && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
+        const uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
+        const uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
+        const uint32_t e_last = __shfl_sync(FULL, e_pos, 31);
+        if (seq_tot != nseq || lit_tot != nl || e_last != bsz) {
+          if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 9u);
+          continue;
+        }
+        // ---------------- pass 2: decode from the true start, write records and literals
+        uint32_t si = seq_inc - seqs, lw = lit_inc - lits_t, run = runin, bad = 0;
+        bool eob_bad = false, saw_eob = false;
+        BitRing<kSpecRing> in;
+        in.init(ring_s, gbits, gmax, S0 + t_start);
+        const uint32_t stop = S0 + e_pos;
+        while (in.at() < stop) {
+          const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+          const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
+          if (islit && lw < nl) lit[lw] = uint8_t(st.byte);
+          lw += islit ? 1u : 0u;
+          run += islit ? 1u : 0u;
+          const bool close = isl || (st.kind == K_EOB && run != 0);
+          if (close && si < nseq) rec[si] = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
+          si += close ? 1u : 0u;
+          run = close ? 0u : run;
+          bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match)) | (st.kind == K_BAD);
+          if (st.kind == K_EOB) { saw_eob = true; eob_bad |= !(last && lane == 31); break; }
+        }
+        const bool at_end = in.at() == stop;
+        in.drain();
+        // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
+        if (bad || eob_bad || !at_end || saw_eob != (last && lane == 31)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
+        continue;
+      }
+    }
+    // ---------------- serial fallback (small sub-blocks, literal runs >= 1023): lane 0 decodes all of it
+    if (lane == 0) {
+      BitRing<kSpecRing> in;
+      in.init(ring_s, gbits, gmax, S0);
+      const uint32_t err = decode_sub_serial<LONG>(in, lut_ll_s, lut_d_s, lmask, sm, a, rec, lit, nseq, nl, last, bsz);
+      in.drain();
+      if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
+    }
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
@@ -771,9 +1044,6 @@ void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
   }
 }
 
-size_t huff_smem_bytes(uint32_t lut_bits, uint32_t nt) {
-  return ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << lut_bits) * sizeof(uint32_t) + size_t(nt) * 128;
-}
 
 gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
                              size_t src_len, uint8_t* d_dst, size_t dst_cap, void* d_ws, size_t ws_bytes,
@@ -826,16 +1096,33 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   while (a.ring_bytes < info->window_size + 4096) a.ring_bytes <<= 1;
   const bool byte_mode = info->mode == GOMP_MODE_BYTE;
   if (!byte_mode && !lz77_only) {
-    // CTA size ~ sub-blocks per block (thread per sub-block), 32..256
-    const uint64_t avg = (uint64_t(info->n_sub_total) + info->n_blocks - 1) / std::max<uint32_t>(info->n_blocks, 1);
-    uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg + 31) / 32 * 32)));
-    const size_t smem = huff_smem_bytes(a.lut_bits, nt);
-    if (info->cwl > a.lut_bits) {
-      cudaFuncSetAttribute(huff_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      huff_decode_kernel<true><<<nblk, nt, smem, st>>>(a);
+    const uint64_t nb = std::max<uint32_t>(info->n_blocks, 1);
+    const uint64_t avg_sub = (uint64_t(info->n_sub_total) + nb - 1) / nb;
+    const uint64_t avg_bits = info->n_sub_total ? (info->file_len - info->payload_base) * 8 / info->n_sub_total : 0;
+    const bool LONGc = info->cwl > a.lut_bits;
+    const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << a.lut_bits) * sizeof(uint32_t);
+    if (avg_bits >= 4 * kSpecMinBits) {
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode
+      const uint32_t nw = uint32_t(std::min<uint64_t>(16, std::max<uint64_t>(1, avg_sub)));
+      const size_t smem = tabs + size_t(nw) * 32 * (kSpecRing * 16 + kRec * 8);
+      if (LONGc) {
+        cudaFuncSetAttribute(huff_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_warp_kernel<true><<<nblk, 32 * nw, smem, st>>>(a);
+      } else {
+        cudaFuncSetAttribute(huff_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_warp_kernel<false><<<nblk, 32 * nw, smem, st>>>(a);
+      }
     } else {
-      cudaFuncSetAttribute(huff_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      huff_decode_kernel<false><<<nblk, nt, smem, st>>>(a);
+      // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block
+      const uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
+      const size_t smem = tabs + size_t(nt) * 128;
+      if (LONGc) {
+        cudaFuncSetAttribute(huff_thread_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_thread_kernel<true><<<nblk, nt, smem, st>>>(a);
+      } else {
+        cudaFuncSetAttribute(huff_thread_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_thread_kernel<false><<<nblk, nt, smem, st>>>(a);
+      }
     }
     if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
   }

@@ -257,3 +257,13 @@ def test_full_size_configs(cfg):
     for b in sorted(set([0, info.n_blocks - 1] + [int(v) for v in rng.integers(0, info.n_blocks, 6)])):
         ref = oracle.decompress_blocks(cn, b, b + 1, bs)
         assert np.array_equal(y[b * bs: b * bs + len(ref)], ref)
+
+
+@pytest.mark.parametrize("kind", ["wiki", "matrix", "nested2", "nested32", "random", "zeros", "text"])
+@pytest.mark.parametrize("k", [1, 4, 16, 40])
+def test_warp_speculative_decode(kind, k):
+    """Long sub-blocks (k per 256 KiB block) take the warp-per-sub-block speculative decoder; incompressible data
+    (1023-literal runs, R10) takes its serial fallback. Output must equal the oracle's bit for bit."""
+    x = _data(kind, 1_500_007, seed=13)
+    c = gomp.compress(x, mode="bit", de=kind != "nested2", block_size=262144, sub_block_seqs=0, sub_blocks_per_block=k)
+    _check(c, x, ["auto"])
