@@ -535,27 +535,21 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
     const uint32_t S0 = uint32_t(sb);        // absolute start bit of the sub-block in the block's bitstream
     bool serial = bsz < kSpecMinBits;
     uint32_t t_start = 0, e_pos = 0, lits_t = 0, nlen_t = 0, lead_t = 0, trail_t = 0, maxrun = 0;
-    bool has_t = false;
+    bool has_t = false, is_tail = false;
     if (!serial) {
       // ---------------- pass 1: speculative scan of this lane's chunk
       const uint32_t c = (bsz + 31) / 32;
       const uint32_t sp = S0 + lane * c;
       const uint32_t lim = S0 + min((lane + 1) * c, bsz);
-      uint32_t lits = 0, nlen = 0, lead = 0, trail = 0, first_len_seen = 0, run = 0, it = 0;
-      uint32_t lead_after_rec = 0xffffffffu;     // literals before the first length code after the recorded range
+      const uint32_t endb = S0 + bsz;
+      uint32_t lits = 0, nlen = 0, lead = 0, run = 0, first_len_seen = 0;
+      uint32_t lead_after_rec = 0xffffffffu;   // literals before the first length code at iteration >= kRec-1
       BitRing<kSpecRing> in;
       in.init(ring_s, gbits, gmax, sp);
-      while (in.at() < lim) {
-        const uint32_t pos = in.at();
-        if (it < kRec) {
-          sts32(recp_s + (it * 32 + lane) * 4, pos - S0);
-          sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
-        }
-        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-        if (st.kind == K_BAD) in.consume(1);    // garbage before self-synchronisation (validated in pass 2)
-        const bool isl = st.kind == K_LEN;
+      auto account = [&](const Step& st, uint32_t it) {
+        if (st.kind == K_BAD) in.consume(1);   // garbage before self-synchronisation (validated in pass 2)
         if (st.kind == K_LIT) { ++lits; ++run; }
-        if (isl) {
+        if (st.kind == K_LEN) {
           if (!first_len_seen) lead = lits;
           if (it + 1 >= kRec && lead_after_rec == 0xffffffffu) lead_after_rec = lits;
           first_len_seen = 1;
@@ -563,88 +557,75 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
           maxrun = max(maxrun, run);
           run = 0;
         }
-        ++it;
+      };
+      // 1a: the first kRec iterations, recording each boundary (position, literals and length codes before it)
+      for (uint32_t it = 0; it < kRec; ++it) {
+        sts32(recp_s + (it * 32 + lane) * 4, in.at() - S0);
+        sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
+        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+        account(st, it);
       }
-      trail = run;
+      __syncwarp();
+      // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there
+      // on both paths are the same (prefix codes: same position, same state => same decode)
+      uint32_t q = lane + 1, ptr = 0, exit_lane = 32, exit_idx = 0;
+      for (uint32_t it = kRec;; ++it) {
+        const uint32_t pos = in.at();
+        if (pos >= endb) break;
+        if (pos >= lim && q < 32) {
+          const uint32_t rel = pos - S0;
+          uint32_t bq = lds32(recp_s + (ptr * 32 + q) * 4);
+          while (bq < rel) {
+            if (++ptr == kRec) { ptr = 0; if (++q == 32) break; }
+            bq = lds32(recp_s + (ptr * 32 + q) * 4);
+          }
+          if (q < 32 && bq == rel) { exit_lane = q; exit_idx = ptr; break; }
+        }
+        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+        account(st, it);
+      }
+      const uint32_t trail = run;
       if (!first_len_seen) lead = lits;
       e_pos = in.at() - S0;
       in.drain();
-      __syncwarp();
-      // ---------------- synchronisation: the true start of lane p is the true exit of lane p-1
-      uint32_t merged = lane == 0 ? 0u : 0xffffffffu;     // recorded index where the true path joins
-      bool fixed = lane == 0;                             // path known to start on the true path
-      for (uint32_t round = 0; round < 33; ++round) {
-        const uint32_t prev_e = __shfl_up_sync(FULL, e_pos, 1);
-        if (!fixed) {
-          merged = 0xffffffffu;
-          const uint32_t rr = min(it, kRec);
-          for (uint32_t r = 0; r < rr; ++r)
-            if (lds32(recp_s + (r * 32 + lane) * 4) == prev_e) { merged = r; break; }
-        }
-        // lane p is on the true path iff every lane before it is: fix the first lane that is not
-        const uint32_t unsynced = __ballot_sync(FULL, merged == 0xffffffffu);
-        if (!unsynced) break;
-        const uint32_t p = __ffs(unsynced) - 1;
-        const uint32_t tstart = __shfl_sync(FULL, e_pos, p - 1);   // true: lanes < p are synced
-        if (lane == p) {
-          const uint32_t lim2 = S0 + min((lane + 1) * c, bsz);
-          lits = 0; nlen = 0; lead = 0; run = 0; first_len_seen = 0; it = 0; lead_after_rec = 0xffffffffu;
-          BitRing<kSpecRing> in2;
-          in2.init(ring_s, gbits, gmax, S0 + tstart);
-          while (in2.at() < lim2) {
-            const uint32_t pos = in2.at();
-            if (it < kRec) {
-              sts32(recp_s + (it * 32 + lane) * 4, pos - S0);
-              sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
-            }
-            const Step st = decode_step<LONG>(in2, lut_ll_s, lut_d_s, lmask, sm);
-            if (st.kind == K_BAD) in2.consume(1);
-            const bool isl = st.kind == K_LEN;
-            if (st.kind == K_LIT) { ++lits; ++run; }
-            if (isl) {
-              if (!first_len_seen) lead = lits;
-              if (it + 1 >= kRec && lead_after_rec == 0xffffffffu) lead_after_rec = lits;
-              first_len_seen = 1;
-              ++nlen;
-              maxrun = max(maxrun, run);
-              run = 0;
-            }
-            ++it;
-          }
-          trail = run;
-          if (!first_len_seen) lead = lits;
-          e_pos = in2.at() - S0;
-          in2.drain();
-          merged = 0;
-          fixed = true;
-        }
-        __syncwarp();
-      }
-      // statistics of the true path = speculative totals minus the prefix before the merge point
-      const uint32_t my_start = lds32(recp_s + (merged * 32 + lane) * 4);
-      const uint32_t cum = lds32(recc_s + (merged * 32 + lane) * 4);
-      const uint32_t lits0 = cum & 0xffffu, nlen0 = cum >> 16;
-      lits_t = lits - lits0;
-      nlen_t = nlen - nlen0;
-      has_t = nlen_t > 0;
-      trail_t = has_t ? trail : lits_t;
-      // literals from the merge point to the first length code after it
-      lead_t = lits_t;
-      if (has_t) {
-        if (nlen0 == 0 && first_len_seen) lead_t = lead - lits0;        // first length code overall is after it
-        else {
-          uint32_t found = 0xffffffffu;
-          const uint32_t rr = min(it, kRec);
-          for (uint32_t r = merged + 1; r < rr; ++r) {
-            const uint32_t cr = lds32(recc_s + (r * 32 + lane) * 4);
-            if ((cr >> 16) > nlen0) { found = r; break; }              // a length code ended before boundary r
-          }
-          // the length code is iteration found-1: literals before it = lits counted at boundary found-1
-          if (found != 0xffffffffu) lead_t = (lds32(recc_s + ((found - 1) * 32 + lane) * 4) & 0xffffu) - lits0;
-          else lead_t = (lead_after_rec != 0xffffffffu ? lead_after_rec : lits) - lits0;
+      // ---------------- the true path: lane 0 starts at the sub-block start (its boundary 0) and hands over to
+      // the lane it exited into, at that lane's recorded boundary; lanes it jumped over own nothing
+      uint32_t merged = 0xffffffffu;   // recorded index where this lane's segment of the true path starts
+      {
+        uint32_t cur = 0, idx = 0;
+        for (uint32_t hop = 0; hop < 32 && cur < 32; ++hop) {
+          if (lane == cur) merged = idx;
+          const uint32_t nl2 = __shfl_sync(FULL, exit_lane, cur), ni = __shfl_sync(FULL, exit_idx, cur);
+          cur = nl2;
+          idx = ni;
         }
       }
-      t_start = my_start;
+      const bool on = merged != 0xffffffffu;
+      is_tail = on && exit_lane == 32;
+      if (on) {
+        // statistics of the true segment = totals at the exit minus the counts before the merge boundary
+        t_start = lds32(recp_s + (merged * 32 + lane) * 4);
+        const uint32_t cum = lds32(recc_s + (merged * 32 + lane) * 4);
+        const uint32_t lits0 = cum & 0xffffu, nlen0 = cum >> 16;
+        lits_t = lits - lits0;
+        nlen_t = nlen - nlen0;
+        has_t = nlen_t > 0;
+        trail_t = has_t ? trail : lits_t;
+        lead_t = lits_t;
+        if (has_t) {
+          if (nlen0 == 0) lead_t = lead - lits0;               // first length code of the path is after it
+          else {
+            uint32_t found = 0xffffffffu;
+            for (uint32_t r = merged + 1; r < kRec; ++r) {
+              if ((lds32(recc_s + (r * 32 + lane) * 4) >> 16) > nlen0) { found = r; break; }  // iteration r-1 was one
+            }
+            if (found != 0xffffffffu) lead_t = (lds32(recc_s + ((found - 1) * 32 + lane) * 4) & 0xffffu) - lits0;
+            else lead_t = (lead_after_rec != 0xffffffffu ? lead_after_rec : lits) - lits0;
+          }
+        }
+      } else {
+        e_pos = t_start = 0;
+      }
       // a literal run of >= 1023 anywhere (R10 closes sequences there): serial fallback for this sub-block
       uint32_t runin = 0;   // run length entering this lane = carried across lanes without length codes
       {
@@ -663,11 +644,11 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
       if (!serial) {
         // ---------------- offsets: exclusive scans of sequences (closed by length codes) and literals
         uint32_t seqs = nlen_t;   // + the EOB-closed final literal-only sequence of the block
-        if (last && lane == 31 && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
+        if (last && is_tail && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
         const uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
         const uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
-        const uint32_t e_last = __shfl_sync(FULL, e_pos, 31);
-        if (seq_tot != nseq || lit_tot != nl || e_last != bsz) {
+        const bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
+        if (seq_tot != nseq || lit_tot != nl || !tail_ok) {
           if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 9u);
           continue;
         }
@@ -688,12 +669,12 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
           si += close ? 1u : 0u;
           run = close ? 0u : run;
           bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match)) | (st.kind == K_BAD);
-          if (st.kind == K_EOB) { saw_eob = true; eob_bad |= !(last && lane == 31); break; }
+          if (st.kind == K_EOB) { saw_eob = true; eob_bad |= !(last && is_tail); break; }
         }
         const bool at_end = in.at() == stop;
         in.drain();
         // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
-        if (bad || eob_bad || !at_end || saw_eob != (last && lane == 31)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
+        if (bad || eob_bad || !at_end || saw_eob != (last && is_tail)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
         continue;
       }
     }
