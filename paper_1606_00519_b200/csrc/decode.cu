@@ -184,51 +184,64 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// LSB-first bit reader of one bitstream segment. The stream is staged through the thread's own ring of NC
-// 16-byte chunks in shared memory by cp.async (LDGSTS), issued NC-1 chunks ahead of use, so no global-load
-// latency sits on the per-symbol dependency chain. The 64-bit window is two registers (lo, hi) and a bit
-// offset: peek() = one funnel shift; consume(n <= 32) crosses at most one word, which costs one shared load.
+// LSB-first bit reader of one bitstream segment, written so that the lanes of a warp never diverge in it.
+// The stream is staged through the thread's own ring of NC 16-byte chunks in shared memory by cp.async
+// (LDGSTS). refill(), called once per decode iteration by every lane, issues (predicated) the next chunk while
+// it is at most NC-2 chunks ahead of the words in use, commits one group and waits until all but the newest
+// kWaitIters groups are complete: a chunk is issued ITS iterations (<= 49 bits each) before its first word is
+// read, so the global-load latency never sits on the per-symbol chain and no lane
+// waits on another lane's data. The 64-bit window is two registers (lo, hi) and a bit offset: peek() = one
+// funnel shift; consume(n <= 32) is branch-free (one shared load, selected when a word boundary is crossed).
 // Chunk addresses are clamped to the file (bytes past the stream are never used).
 template <uint32_t NC>
 struct BitRing {
   static constexpr uint32_t WM = NC * 4 - 1;   // word mask of the ring
+  // a chunk issued at iteration i is first read >= 32*(4*(NC-2)-3) bits later, i.e. at iteration >= i+ITS
+  // (<= 49 bits per iteration), so the wait in iteration i+ITS-1 may leave the ITS-1 newest groups pending
+  static constexpr uint32_t ITS = (32 * (4 * (NC - 2) - 3) + 48) / 49;
+  static constexpr uint32_t kWaitIters = ITS - 1;
   uint32_t ring;                               // shared-window address of this thread's ring
   const uint8_t* gbase;                        // 16-aligned start of the block's bitstream
   uint64_t gmax;                               // last valid 16-byte chunk offset from gbase
-  uint32_t w, w0, lo, hi, pos, pos0;
-  __device__ __forceinline__ void issue(uint32_t c) {
+  uint32_t w, lo, hi, pos, nextc;
+  __device__ __forceinline__ const uint8_t* chunk_addr(uint32_t c) const {
     const uint64_t off = uint64_t(c) * 16u;
-    cp_async16(ring + (c % NC) * 16u, gbase + (off <= gmax ? off : gmax));
-    cp_commit();
+    return gbase + (off <= gmax ? off : gmax);
   }
   __device__ __forceinline__ void init(uint32_t r, const uint8_t* gb, uint64_t gm, uint32_t start) {
     ring = r;
     gbase = gb;
     gmax = gm;
-    w0 = w = start >> 5;
-    pos0 = pos = start & 31;
-    const uint32_t c0 = w0 >> 2;
+    w = start >> 5;
+    pos = start & 31;
+    const uint32_t c0 = w >> 2;
 #pragma unroll
-    for (uint32_t k = 0; k + 1 < NC; ++k) issue(c0 + k);
-    cp_wait_n<NC - 2>();                                       // chunk c0 landed
-    if ((w0 & 3u) == 3u) { issue(c0 + NC - 1); cp_wait_n<NC - 2>(); }   // hi lies in chunk c0 + 1
-    lo = lds32(ring + ((w0 & WM) << 2));
-    hi = lds32(ring + (((w0 + 1) & WM) << 2));
+    for (uint32_t k = 0; k + 1 < NC; ++k) cp_async16(ring + ((c0 + k) % NC) * 16u, chunk_addr(c0 + k));
+    cp_commit();
+    cp_wait_n<0>();
+    nextc = c0 + NC - 1;
+    lo = lds32(ring + ((w & WM) << 2));
+    hi = lds32(ring + (((w + 1) & WM) << 2));
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
   __device__ __forceinline__ void consume(uint32_t n) {
     pos += n;
-    if (pos >= 32) {
-      pos -= 32;
-      ++w;
-      lo = hi;
-      const uint32_t nw = w + 1;
-      if ((nw & 3u) == 0) {                                    // entering chunk nw/4: top up, wait for it
-        issue((nw >> 2) + NC - 2);
-        cp_wait_n<NC - 2>();
-      }
-      hi = lds32(ring + ((nw & WM) << 2));
-    }
+    const bool c = pos >= 32;
+    pos -= c ? 32u : 0u;
+    w += c ? 1u : 0u;
+    const uint32_t nh = lds32(ring + (((w + 1) & WM) << 2));
+    lo = c ? hi : lo;
+    hi = c ? nh : hi;
+  }
+  __device__ __forceinline__ void refill() {
+    const uint32_t p = nextc <= ((w + 1) >> 2) + NC - 2 ? 1u : 0u;
+    const uint32_t sa = ring + (nextc % NC) * 16u;
+    const uint8_t* ga = chunk_addr(nextc);
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q cp.async.cg.shared.global [%0], [%1], 16;\n}\n"
+                 ::"r"(sa), "l"(ga), "r"(p) : "memory");
+    nextc += p;
+    cp_commit();
+    cp_wait_n<kWaitIters>();
   }
   __device__ __forceinline__ uint32_t at() const { return w * 32 + pos; }  // absolute bit position
   __device__ __forceinline__ void drain() const { cp_wait_n<0>(); }
@@ -243,6 +256,7 @@ template <bool LONG, class BR>
 __device__ __forceinline__ Step decode_step(BR& in, uint32_t lut_ll_s, uint32_t lut_d_s, uint32_t lmask,
                                             const HuffSmem& sm) {
   Step st;
+  in.refill();
   const uint32_t pk = in.peek();
   uint32_t ent = lds32(lut_ll_s + ((pk & lmask) << 2));
   uint32_t len = ent & 15u;
@@ -547,16 +561,16 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
       BitRing<kSpecRing> in;
       in.init(ring_s, gbits, gmax, sp);
       auto account = [&](const Step& st, uint32_t it) {
-        if (st.kind == K_BAD) in.consume(1);   // garbage before self-synchronisation (validated in pass 2)
-        if (st.kind == K_LIT) { ++lits; ++run; }
-        if (st.kind == K_LEN) {
-          if (!first_len_seen) lead = lits;
-          if (it + 1 >= kRec && lead_after_rec == 0xffffffffu) lead_after_rec = lits;
-          first_len_seen = 1;
-          ++nlen;
-          maxrun = max(maxrun, run);
-          run = 0;
-        }
+        in.consume(st.kind == K_BAD ? 1u : 0u);   // garbage before self-synchronisation (validated in pass 2)
+        const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
+        lits += islit ? 1u : 0u;
+        run += islit ? 1u : 0u;
+        lead = (isl && !first_len_seen) ? lits : lead;
+        lead_after_rec = (isl && it + 1 >= kRec && lead_after_rec == 0xffffffffu) ? lits : lead_after_rec;
+        first_len_seen |= isl ? 1u : 0u;
+        nlen += isl ? 1u : 0u;
+        maxrun = isl ? max(maxrun, run) : maxrun;
+        run = isl ? 0u : run;
       };
       // 1a: the first kRec iterations, recording each boundary (position, literals and length codes before it)
       for (uint32_t it = 0; it < kRec; ++it) {
