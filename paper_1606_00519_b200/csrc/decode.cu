@@ -488,11 +488,11 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
 // scans give every lane its record and literal offsets and pass 2 decodes again from the true starts, writing
 // records and literals. Sequences close only at length codes here (a literal run reaching 1023 bytes, R10,
 // makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
-constexpr uint32_t kRec = 12;            // recorded iteration boundaries per lane (self-sync window)
+constexpr uint32_t kRec = 32;            // recorded iteration boundaries per lane (self-sync window)
 constexpr uint32_t kSpecRing = 4;        // 16-byte chunks per lane bit ring
 constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this use one lane (serial)
 
-__host__ __device__ constexpr uint32_t spec_warp_bytes() { return 32 * (kSpecRing * 16 + kRec * 8); }
+__host__ __device__ constexpr uint32_t spec_warp_bytes() { return 32 * (kSpecRing * 16 + kRec * 4); }
 
 template <bool LONG>
 __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
@@ -504,8 +504,8 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t wbase_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + warp * spec_warp_bytes();
   const uint32_t ring_s = wbase_s + lane * (kSpecRing * 16);           // this lane's bit ring
-  const uint32_t recp_s = wbase_s + 32 * kSpecRing * 16;               // [kRec][32] boundary positions
-  const uint32_t recc_s = recp_s + kRec * 32 * 4;                      // [kRec][32] lits | nlen << 16 before it
+  // [kRec][32] recorded boundaries: (position - lane start) | literals before it << 16 | length codes << 24
+  const uint32_t recs_s = wbase_s + 32 * kSpecRing * 16;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
   if (!huff_block_ok(a, e, block_ulen(a, b))) {
@@ -574,8 +574,7 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
       };
       // 1a: the first kRec iterations, recording each boundary (position, literals and length codes before it)
       for (uint32_t it = 0; it < kRec; ++it) {
-        sts32(recp_s + (it * 32 + lane) * 4, in.at() - S0);
-        sts32(recc_s + (it * 32 + lane) * 4, lits | (nlen << 16));
+        sts32(recs_s + (it * 32 + lane) * 4, (in.at() - sp) | (lits << 16) | (nlen << 24));
         const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
         account(st, it);
       }
@@ -588,10 +587,10 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
         if (pos >= endb) break;
         if (pos >= lim && q < 32) {
           const uint32_t rel = pos - S0;
-          uint32_t bq = lds32(recp_s + (ptr * 32 + q) * 4);
+          uint32_t bq = q * c + (lds32(recs_s + (ptr * 32 + q) * 4) & 0xffffu);
           while (bq < rel) {
             if (++ptr == kRec) { ptr = 0; if (++q == 32) break; }
-            bq = lds32(recp_s + (ptr * 32 + q) * 4);
+            bq = q * c + (lds32(recs_s + (ptr * 32 + q) * 4) & 0xffffu);
           }
           if (q < 32 && bq == rel) { exit_lane = q; exit_idx = ptr; break; }
         }
@@ -618,9 +617,9 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
       is_tail = on && exit_lane == 32;
       if (on) {
         // statistics of the true segment = totals at the exit minus the counts before the merge boundary
-        t_start = lds32(recp_s + (merged * 32 + lane) * 4);
-        const uint32_t cum = lds32(recc_s + (merged * 32 + lane) * 4);
-        const uint32_t lits0 = cum & 0xffffu, nlen0 = cum >> 16;
+        const uint32_t cum = lds32(recs_s + (merged * 32 + lane) * 4);
+        t_start = lane * c + (cum & 0xffffu);
+        const uint32_t lits0 = (cum >> 16) & 0xffu, nlen0 = cum >> 24;
         lits_t = lits - lits0;
         nlen_t = nlen - nlen0;
         has_t = nlen_t > 0;
@@ -631,9 +630,9 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
           else {
             uint32_t found = 0xffffffffu;
             for (uint32_t r = merged + 1; r < kRec; ++r) {
-              if ((lds32(recc_s + (r * 32 + lane) * 4) >> 16) > nlen0) { found = r; break; }  // iteration r-1 was one
+              if ((lds32(recs_s + (r * 32 + lane) * 4) >> 24) > nlen0) { found = r; break; }  // iteration r-1 was one
             }
-            if (found != 0xffffffffu) lead_t = (lds32(recc_s + ((found - 1) * 32 + lane) * 4) & 0xffffu) - lits0;
+            if (found != 0xffffffffu) lead_t = ((lds32(recs_s + ((found - 1) * 32 + lane) * 4) >> 16) & 0xffu) - lits0;
             else lead_t = (lead_after_rec != 0xffffffffu ? lead_after_rec : lits) - lits0;
           }
         }
@@ -1099,7 +1098,7 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     if (avg_bits >= 4 * kSpecMinBits) {
       // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode
       const uint32_t nw = uint32_t(std::min<uint64_t>(16, std::max<uint64_t>(1, avg_sub)));
-      const size_t smem = tabs + size_t(nw) * 32 * (kSpecRing * 16 + kRec * 8);
+      const size_t smem = tabs + size_t(nw) * spec_warp_bytes();
       if (LONGc) {
         cudaFuncSetAttribute(huff_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         huff_warp_kernel<true><<<nblk, 32 * nw, smem, st>>>(a);
