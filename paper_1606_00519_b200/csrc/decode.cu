@@ -815,52 +815,77 @@ __device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint3
   return true;
 }
 
-// DE group as byte rows (a6 + a7 fused). Group-relative positions x in [0, T) (T = group output bytes).
+// DE group as word rows (a6 + a7 fused). Group-relative positions x in [0, T) (T = group output bytes).
 // Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte x is lring[x + ld_i], match part
 // [dst_i, opr_{i+1}) whose byte x is (own_i ? lring : ring)[x + md_i] (own_i: source inside its own literal,
-// reading R4). Under the DE rule no source lies in this group's output, so the group is computed in rows of
-// 32 consecutive bytes, lane t owning byte base + t. Row r's sequence starts are word r of a shared bitmap
-// (set with one ATOMS.OR per lane), so the owner of byte x is c0 + popc(bits <= lane) - 1; its descriptor is
-// one broadcast 16-byte shared load. Four rows per step: every load of a step precedes its stores (sources
-// never lie in this group's output). Uniform control flow, no inter-lane ordering (P:295-329 at byte level).
-__device__ __forceinline__ void de_group_rows(uint32_t ring, uint32_t RM, uint32_t lring, uint32_t LM,
-                                              uint32_t prm, uint32_t bits, uint32_t lane, bool act, bool has,
-                                              uint32_t opr, uint32_t lit, uint32_t lpos, uint32_t dist, bool own,
-                                              uint32_t o, uint32_t T) {
-  const uint32_t dstr = opr + lit;
+// reading R4). Under the DE rule no source lies in this group's output, so every output word is a function of
+// final on-chip data: the group is written as rows of 32 aligned 32-bit words (lane t -> word t of the row).
+// The owner of a word's first byte comes from a bitmap of sequence starts (one RED.OR per lane) and popcounts;
+// a word touches at most two sequences, i.e. at most four segments (literal/match of the owner and of its
+// successor); each present segment contributes one funnel-shifted source word under a byte mask. Bytes of the
+// first word that precede the group are kept from the ring (final); bytes past the group in the last word are
+// rewritten by the next group. No inter-lane ordering, no divergence beyond predication.
+__device__ __forceinline__ uint32_t ring_word_at(uint32_t base, uint32_t mask, uint32_t p) {
+  const uint32_t i = p & ~3u;
+  return __funnelshift_r(lds32(base + (i & mask)), lds32(base + ((i + 4) & mask)), (p & 3u) * 8u);
+}
+__device__ __forceinline__ uint32_t byte_mask(int32_t a, int32_t b) {   // bytes [a, b) of a word, 0 <= a < b <= 4
+  return (0xffffffffu >> (32 - 8 * (b - a))) << (8 * a);
+}
+__device__ __forceinline__ void de_group_words(uint32_t ring, uint32_t RM, uint32_t lring, uint32_t LM,
+                                               uint32_t prm, uint32_t bits, uint32_t lane, bool act, bool has,
+                                               uint32_t opr, uint32_t lit, uint32_t lpos, uint32_t dist, bool own,
+                                               uint32_t o, uint32_t T) {
+  const uint32_t ob = o & 3u;                                      // group start within its first word
   const uint32_t ld = lpos - opr;                                  // lring position of byte x = x + ld
   const bool own_ = has && own;
   const uint32_t md = own_ ? ld - dist : o - dist;                 // match source position = x + md
-  sts128(prm + lane * 16, make_uint4(opr, dstr | (own_ ? 0x80000000u : 0u), ld, md));
-  if (act) ats_or(bits + (opr >> 5) * 4, 1u << (opr & 31));
+  // descriptor: start, literal end | own << 31, literal delta, match delta (inactive lanes: start = T)
+  sts128(prm + lane * 16, make_uint4(opr, (opr + lit) | (own_ ? 0x80000000u : 0u), ld, md));
+  if (act) ats_or(bits + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
   __syncwarp();
-  const uint32_t le = (2u << lane) - 1u;                           // lanes <= this lane
+  const uint32_t nwords = (ob + T + 3) >> 2, wbase = o >> 2;
   uint32_t c0 = 0;                                                 // sequences starting before the row
-  for (uint32_t base0 = 0; base0 < T; base0 += 128) {
-    const uint4 Mv = lds128(bits + (base0 >> 5) * 4);
-    const uint32_t Ms[4] = {Mv.x, Mv.y, Mv.z, Mv.w};
-    uint32_t byte[4];
+  for (uint32_t k0 = 0; k0 < nwords; k0 += 32) {
+    const uint4 W = lds128(bits + (k0 >> 3) * 4);                  // the row's 128 bitmap bits
+    const uint32_t p0 = __popc(W.x), p1 = __popc(W.y), p2 = __popc(W.z), p3 = __popc(W.w);
+    const uint32_t k = k0 + lane;
+    const int32_t x0 = int32_t(4 * k) - int32_t(ob);
+    if (k < nwords) {
+      const uint32_t ry = (x0 < 0 ? ob : uint32_t(x0) + ob) - 4 * k0;   // row-relative bit of the first byte in
+      const uint32_t q = ry >> 5;
+      const uint32_t Wq = q == 0 ? W.x : q == 1 ? W.y : q == 2 ? W.z : W.w;
+      const uint32_t pre = (q > 0 ? p0 : 0u) + (q > 1 ? p1 : 0u) + (q > 2 ? p2 : 0u);
+      const uint32_t j = c0 + pre + __popc(Wq & ((2u << (ry & 31)) - 1u)) - 1u;
+      const uint4 P = lds128(prm + j * 16);
+      const uint4 Q = lds128(prm + (j < 31 ? j + 1 : 31) * 16);
+      const int32_t pdst = int32_t(P.y & 0x7fffffffu);
+      const int32_t nst = j < 31 ? int32_t(Q.x) : int32_t(T);
+      const int32_t qdst = j < 31 ? int32_t(Q.y & 0x7fffffffu) : int32_t(T);
+      const int32_t xe = min(x0 + 4, int32_t(T));
+      const int32_t xs = max(x0, 0);
+      uint32_t val = x0 < 0 ? lds32(ring + ((4 * (wbase + k)) & RM)) : 0u;
+      // four candidate segments: [lo, hi) with source delta and source ring
+      const int32_t lo4[4] = {xs, pdst, nst, qdst};
+      const int32_t hi4[4] = {pdst, nst, qdst, int32_t(T)};
+      const uint32_t dl4[4] = {P.z, P.w, Q.z, Q.w};
+      const bool fl4[4] = {true, (P.y >> 31) != 0, true, (Q.y >> 31) != 0};
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t x = base0 + 32 * r + lane;
-      const uint32_t j = c0 + __popc(Ms[r] & le) - 1u;
-      c0 += __popc(Ms[r]);
-      byte[r] = 0;
-      if (x < T) {
-        const uint4 D = lds128(prm + j * 16);
-        const bool in_lit = x < (D.y & 0x7fffffffu);
-        const uint32_t p = x + (in_lit ? D.z : D.w);
-        byte[r] = (in_lit || (D.y >> 31)) ? lds8(lring + (p & LM)) : lds8(ring + (p & RM));
+      for (int sg = 0; sg < 4; ++sg) {
+        const int32_t s0 = max(lo4[sg], xs), s1 = min(hi4[sg], xe);
+        if (s0 < s1) {
+          const uint32_t m = byte_mask(s0 - x0, s1 - x0);
+          const uint32_t pos = uint32_t(x0) + dl4[sg];
+          const uint32_t v = fl4[sg] ? ring_word_at(lring, LM, pos) : ring_word_at(ring, RM, pos);
+          val = (val & ~m) | (v & m);
+        }
       }
+      sts32(ring + ((4 * (wbase + k)) & RM), val);
     }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t x = base0 + 32 * r + lane;
-      if (x < T) sts8(ring + ((o + x) & RM), byte[r]);
-    }
+    c0 += p0 + p1 + p2 + p3;
   }
   // clear the bitmap words this group used (the group-end __syncwarp orders this before the next group)
-  for (uint32_t wd = lane; wd < (T + 31) / 32; wd += 32) sts32(bits + wd * 4, 0u);
+  for (uint32_t wd = lane; wd < (ob + T + 31) / 32; wd += 32) sts32(bits + wd * 4, 0u);
 }
 
 __device__ __forceinline__ void cp_wait(uint32_t allowed) {
@@ -960,8 +985,8 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
         // group's output rows, balanced over the lanes, with no inter-lane ordering at all.
         const bool de_ok = !has || src + L <= o_carry || src >= op;
         if (__all_sync(FULL, de_ok)) {
-          de_group_rows(ring, RM, lring, LM, prm, bits, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
-                        o_carry, out_sum);
+          de_group_words(ring, RM, lring, LM, prm, bits, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
+                         o_carry, out_sum);
           if (STATS) {
             const uint32_t any = __ballot_sync(FULL, has);
             uint32_t bytes = has ? L : 0u;
