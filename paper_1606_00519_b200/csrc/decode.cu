@@ -715,6 +715,7 @@ constexpr uint32_t kLitRing = 2048;
 constexpr uint32_t kLitUnit = 512;    // 32 lanes x 16 B per cp.async instruction
 constexpr uint32_t kLitAhead = 1024;  // prefetch distance in literal bytes
 constexpr uint32_t kPrmBytes = 32 * 16;  // the group's 32 sequence descriptors (DE pass)
+constexpr uint32_t kFlushBytes = 2048;   // ring -> HBM flush granularity
 
 // per-warp shared layout: [ring RING][literal ring 2 KiB][descriptors 512 B][row-start bitmap RING/8 B]
 __host__ __device__ constexpr uint32_t lz_warp_bytes(uint32_t ring) { return ring + kLitRing + kPrmBytes + ring / 8; }
@@ -854,8 +855,10 @@ __device__ __forceinline__ void de_group_words(uint32_t ring, uint32_t RM, uint3
     if (k < nwords) {
       const uint32_t ry = (x0 < 0 ? ob : uint32_t(x0) + ob) - 4 * k0;   // row-relative bit of the first byte in
       const uint32_t q = ry >> 5;
-      const uint32_t Wq = q == 0 ? W.x : q == 1 ? W.y : q == 2 ? W.z : W.w;
-      const uint32_t pre = (q > 0 ? p0 : 0u) + (q > 1 ? p1 : 0u) + (q > 2 ? p2 : 0u);
+      uint32_t Wq = W.x, pre = 0;
+      Wq = q >= 1 ? W.y : Wq; pre += q >= 1 ? p0 : 0u;
+      Wq = q >= 2 ? W.z : Wq; pre += q >= 2 ? p1 : 0u;
+      Wq = q >= 3 ? W.w : Wq; pre += q >= 3 ? p2 : 0u;
       const uint32_t j = c0 + pre + __popc(Wq & ((2u << (ry & 31)) - 1u)) - 1u;
       const uint4 P = lds128(prm + j * 16);
       const uint4 Q = lds128(prm + (j < 31 ? j + 1 : 31) * 16);
@@ -864,8 +867,8 @@ __device__ __forceinline__ void de_group_words(uint32_t ring, uint32_t RM, uint3
       const int32_t qdst = j < 31 ? int32_t(Q.y & 0x7fffffffu) : int32_t(T);
       const int32_t xe = min(x0 + 4, int32_t(T));
       const int32_t xs = max(x0, 0);
-      uint32_t val = x0 < 0 ? lds32(ring + ((4 * (wbase + k)) & RM)) : 0u;
-      // four candidate segments: [lo, hi) with source delta and source ring
+      uint32_t val = lds32(ring + ((4 * (wbase + k)) & RM));   // keeps the bytes before the group (x0 < 0)
+      // four candidate segments [lo, hi) with source delta and ring; all evaluated, empty ones masked out
       const int32_t lo4[4] = {xs, pdst, nst, qdst};
       const int32_t hi4[4] = {pdst, nst, qdst, int32_t(T)};
       const uint32_t dl4[4] = {P.z, P.w, Q.z, Q.w};
@@ -873,19 +876,19 @@ __device__ __forceinline__ void de_group_words(uint32_t ring, uint32_t RM, uint3
 #pragma unroll
       for (int sg = 0; sg < 4; ++sg) {
         const int32_t s0 = max(lo4[sg], xs), s1 = min(hi4[sg], xe);
-        if (s0 < s1) {
-          const uint32_t m = byte_mask(s0 - x0, s1 - x0);
-          const uint32_t pos = uint32_t(x0) + dl4[sg];
-          const uint32_t v = fl4[sg] ? ring_word_at(lring, LM, pos) : ring_word_at(ring, RM, pos);
-          val = (val & ~m) | (v & m);
-        }
+        const uint32_t m = s0 < s1 ? byte_mask(s0 - x0, s1 - x0) : 0u;
+        const uint32_t pos = uint32_t(x0) + dl4[sg];
+        const uint32_t base = fl4[sg] ? lring : ring, msk = fl4[sg] ? LM : RM;
+        const uint32_t v = ring_word_at(base, msk, pos);
+        val = (val & ~m) | (v & m);
       }
       sts32(ring + ((4 * (wbase + k)) & RM), val);
     }
     c0 += p0 + p1 + p2 + p3;
   }
-  // clear the bitmap words this group used (the group-end __syncwarp orders this before the next group)
-  for (uint32_t wd = lane; wd < (ob + T + 31) / 32; wd += 32) sts32(bits + wd * 4, 0u);
+  // clear the bitmap words this group used, 4 per store (the group-end __syncwarp orders this before the next
+  // group's RED.OR)
+  for (uint32_t wd = 4 * lane; wd < (ob + T + 31) / 32; wd += 128) sts128(bits + wd * 4, make_uint4(0u, 0u, 0u, 0u));
 }
 
 __device__ __forceinline__ void cp_wait(uint32_t allowed) {
@@ -964,7 +967,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       return;
     }
     const bool has = act && L;
-    const bool fast = out_sum + a.window + 16 <= RING && lit_sum + kLitAhead <= kLitRing;
+    // fast path: the group and the window fit the ring, and the group does not overwrite unflushed output
+    const bool fast = out_sum + a.window + 16 <= RING && o_carry + out_sum - flushed <= RING &&
+                      lit_sum + kLitAhead <= kLitRing;
     if (fast) {
       // stage the group's literals (rel range [lofs + l_carry, need)) into the literal ring
       const uint32_t need = lofs + l_carry + lit_sum;
@@ -1009,11 +1014,13 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
         if (!resolve_group<S2, STATS>(a, ro, lane, has, dst, src, L, op, b, g0)) return;
       }
       __syncwarp();
-      // flush completed 16-byte chunks to HBM (coalesced 16-byte stores)
+      // flush completed 16-byte chunks to HBM (coalesced 16-byte stores), at least kFlushBytes at a time
       const uint32_t q1 = (o_carry + out_sum) >> 4;
-      for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
-        reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
-      if (q1 * 16 > flushed) flushed = q1 * 16;
+      if (q1 * 16 >= flushed + kFlushBytes) {
+        for (uint32_t q = (flushed >> 4) + lane; q < q1; q += 32)
+          reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
+        flushed = q1 * 16;
+      }
     } else {
       // group too large for the rings: flush the ring, run the group in global memory, reload the window
       __syncwarp();
