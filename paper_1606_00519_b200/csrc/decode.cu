@@ -575,8 +575,10 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
       // 1a: the first kRec iterations, recording each boundary (position, literals and length codes before it)
       for (uint32_t it = 0; it < kRec; ++it) {
         sts32(recs_s + (it * 32 + lane) * 4, (in.at() - sp) | (lits << 16) | (nlen << 24));
-        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-        account(st, it);
+        if (in.at() < endb) {                    // never decode past the end of the sub-block
+          const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
+          account(st, it);
+        }
       }
       __syncwarp();
       // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there

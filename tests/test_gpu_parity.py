@@ -260,10 +260,19 @@ def test_full_size_configs(cfg):
 
 
 @pytest.mark.parametrize("kind", ["wiki", "matrix", "nested2", "nested32", "random", "zeros", "text"])
-@pytest.mark.parametrize("k", [1, 4, 16, 40])
+@pytest.mark.parametrize("k", [1, 4, 16, 40, 64])
 def test_warp_speculative_decode(kind, k):
     """Long sub-blocks (k per 256 KiB block) take the warp-per-sub-block speculative decoder; incompressible data
     (1023-literal runs, R10) takes its serial fallback. Output must equal the oracle's bit for bit."""
     x = _data(kind, 1_500_007, seed=13)
     c = gomp.compress(x, mode="bit", de=kind != "nested2", block_size=262144, sub_block_seqs=0, sub_blocks_per_block=k)
+    _check(c, x, ["auto"])
+
+
+@pytest.mark.parametrize("kind", ["wiki", "matrix", "text", "nested8"])
+@pytest.mark.parametrize("bs,k", [(65536, 16), (65536, 4), (131072, 24), (1 << 20, 16)])
+def test_warp_speculative_short_chunks(kind, bs, k):
+    """Sub-blocks whose 32 lane chunks hold fewer symbols than the self-sync window (kRec)."""
+    x = _data(kind, 2_000_003, seed=21)
+    c = gomp.compress(x, mode="bit", de=True, block_size=bs, sub_block_seqs=0, sub_blocks_per_block=k)
     _check(c, x, ["auto"])
