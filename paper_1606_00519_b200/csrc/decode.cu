@@ -202,16 +202,15 @@ struct BitRing {
   static constexpr uint32_t kWaitIters = ITS - 1;
   uint32_t ring;                               // shared-window address of this thread's ring
   const uint8_t* gbase;                        // 16-aligned start of the block's bitstream
-  uint64_t gmax;                               // last valid 16-byte chunk offset from gbase
+  uint32_t gmax;                               // last valid 16-byte chunk offset from gbase
   uint32_t w, lo, hi, pos, nextc;
   __device__ __forceinline__ const uint8_t* chunk_addr(uint32_t c) const {
-    const uint64_t off = uint64_t(c) * 16u;
-    return gbase + (off <= gmax ? off : gmax);
+    return gbase + min(c * 16u, gmax);
   }
   __device__ __forceinline__ void init(uint32_t r, const uint8_t* gb, uint64_t gm, uint32_t start) {
     ring = r;
     gbase = gb;
-    gmax = gm;
+    gmax = uint32_t(gm < 0xfffffff0ull ? gm : 0xfffffff0ull);
     w = start >> 5;
     pos = start & 31;
     const uint32_t c0 = w >> 2;
@@ -668,7 +667,11 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
           continue;
         }
         // ---------------- pass 2: decode from the true start, write records and literals
-        uint32_t si = seq_inc - seqs, lw = lit_inc - lits_t, run = runin, bad = 0;
+        uint32_t run = runin, bad = 0;
+        uint32_t* rp = rec + (seq_inc - seqs);
+        uint32_t* const rend = rec + nseq;
+        uint8_t* lp = lit + (lit_inc - lits_t);
+        uint8_t* const lend = lit + nl;
         bool eob_bad = false, saw_eob = false;
         BitRing<kSpecRing> in;
         in.init(ring_s, gbits, gmax, S0 + t_start);
@@ -676,12 +679,12 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
         while (in.at() < stop) {
           const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
           const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
-          if (islit && lw < nl) lit[lw] = uint8_t(st.byte);
-          lw += islit ? 1u : 0u;
+          if (islit && lp < lend) *lp = uint8_t(st.byte);
+          lp += islit ? 1 : 0;
           run += islit ? 1u : 0u;
           const bool close = isl || (st.kind == K_EOB && run != 0);
-          if (close && si < nseq) rec[si] = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
-          si += close ? 1u : 0u;
+          if (close && rp < rend) *rp = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
+          rp += close ? 1 : 0;
           run = close ? 0u : run;
           bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match)) | (st.kind == K_BAD);
           if (st.kind == K_EOB) { saw_eob = true; eob_bad |= !(last && is_tail); break; }
