@@ -1062,6 +1062,250 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
 
 size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * lz_warp_bytes(ring); }
 
+// ------------------------------------------------------------------ K2b: several warps per data block (DE)
+//
+// One warp per data block (the paper's mapping) leaves a B200 SM with ~7 LZ77 warps at BASELINE C2
+// (1024 blocks), so every group pays the full latency of its dependent chain. Here kBW warps of one CTA take
+// kBW consecutive DE groups of the same block at once (a "batch"). Under the DE rule a group's sources lie
+// below its own start (or in its own literal), but they may lie in an EARLIER group of the same batch, which
+// is being written concurrently: such a byte is resolved by chasing — locate the source position in that
+// group's descriptors (sequence-start bitmap + prefix counts + 16-byte descriptor) and continue from its source
+// (a literal byte, or a position further back) until it lands below the batch start (final in the output ring)
+// or in a literal. Each hop goes to a strictly earlier group, so at most kBW-1 hops. No inter-warp ordering
+// inside a batch; three CTA barriers per batch.
+constexpr uint32_t kBW = 4;                     // warps (groups in flight) per data block
+constexpr uint32_t kGrpMaxOut = 4096;           // fast path: group output + start offset within its word
+constexpr uint32_t kLbuf = 1024;                // per-group literal staging buffer (fast path: lit_sum <= 1008)
+constexpr uint32_t kGrpBitWords = kGrpMaxOut / 32;
+constexpr uint32_t kSlot = 512 + 2 * kGrpBitWords * 4 + kLbuf;   // descriptors | bitmap | prefix counts | literals
+
+__host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kBW * kSlot + kBW * 16 + kBW * 16; }
+
+struct BatchView {
+  uint32_t ring, RM, slot0, oB;
+  uint32_t og[kBW];
+};
+
+// value of output byte q (absolute in the block) of the current batch: chase through earlier groups
+__device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
+#pragma unroll 1
+  for (uint32_t hop = 0; hop < kBW; ++hop) {
+    if (q < v.oB) return lds8(v.ring + (q & v.RM));
+    uint32_t h = 0;
+#pragma unroll
+    for (uint32_t hh = 1; hh < kBW; ++hh) h = v.og[hh] <= q ? hh : h;
+    const uint32_t hs = v.slot0 + h * kSlot;
+    const uint32_t xr = q - v.og[h], y = xr + (v.og[h] & 3u);
+    const uint32_t bw = lds32(hs + 512 + (y >> 5) * 4), pc = lds32(hs + 512 + kGrpBitWords * 4 + (y >> 5) * 4);
+    const uint32_t j = pc + __popc(bw & ((2u << (y & 31)) - 1u)) - 1u;
+    const uint4 D = lds128(hs + j * 16);
+    if (xr < (D.y & 0x7fffffffu)) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.z);
+    if (D.y >> 31) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.w);
+    q -= D.w;
+  }
+  return lds8(v.ring + (q & v.RM));
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int byte_mode) {
+  extern __shared__ __align__(16) uint8_t bz[];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
+  const uint32_t RING = a.ring_bytes, RM = RING - 1;
+  const uint32_t ring = uint32_t(__cvta_generic_to_shared(bz));
+  const uint32_t slot0 = ring + RING;
+  const uint32_t prm_s = slot0 + w * kSlot, bits_s = prm_s + 512, pcnt_s = bits_s + kGrpBitWords * 4,
+                 lbuf_s = pcnt_s + kGrpBitWords * 4;
+  const uint32_t tab = slot0 + kBW * kSlot, flg = tab + kBW * 16;
+  sts128(bits_s + lane * 16, make_uint4(0u, 0u, 0u, 0u));          // 128 bitmap words of this warp
+  const BlockEntry e = load_entry(a.src, b, lane);
+  const uint32_t ulen = block_ulen(a, b);
+  const uint8_t* base;
+  bool ok = e.n_lit <= ulen && e.n_seq <= ulen;
+  if (byte_mode) {
+    ok = ok && payload_ok(a, e) && 4ull * e.n_seq + e.n_lit <= e.payload_len && e.S == 0 && e.n_sub == 0 && e.sub_first == 0;
+    base = a.src + e.payload_off;
+  } else {
+    ok = ok && 4ull * e.n_seq + e.n_lit <= a.max_tok;
+    base = a.tokens + uint64_t(bi) * a.tok_stride;
+  }
+  if (!ok) {
+    if (threadIdx.x == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 1);
+    return;
+  }
+  const uint32_t* recs = reinterpret_cast<const uint32_t*>(base);
+  const uint8_t* lits = base + 4ull * e.n_seq;
+  uint8_t* out = a.dst + uint64_t(bi) * a.block_size;
+  const uint32_t mm1 = a.min_match - 1, n_seq = e.n_seq, ngroups = (n_seq + 31) / 32;
+  const GlobalOut go{out};
+  uint32_t oB = 0, lB = 0, flushed = 0;
+  uint32_t r_next = (w * 32 + lane) < n_seq ? __ldg(recs + w * 32 + lane) : 0u;
+  __syncthreads();
+  for (uint32_t B0 = 0; B0 < ngroups; B0 += kBW) {
+    const uint32_t g = B0 + w, i = g * 32 + lane;
+    const bool act = i < n_seq;
+    const uint32_t r = r_next;
+    r_next = (i + 32 * kBW) < n_seq ? __ldg(recs + i + 32 * kBW) : 0u;
+    // a5: record decode + packed scan of this warp's group
+    const uint32_t lit = r & 1023u, mcode = (r >> 10) & 63u, dist = (r >> 16) + 1u;
+    const uint32_t L = mcode ? mcode + mm1 : 0u;
+    const uint32_t v = lit | ((lit + L) << 16);
+    const uint32_t incl = warp_incl_scan_u32(v, lane);
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    const uint32_t ex = incl - v;
+    const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
+    if (lane == 0) sts128(tab + w * 16, make_uint4(out_sum, lit_sum, 0u, 0u));
+    __syncthreads();
+    // batch offsets of every group (all warps compute all of them)
+    BatchView bv;
+    bv.ring = ring; bv.RM = RM; bv.slot0 = slot0; bv.oB = oB;
+    uint32_t og = oB, lg = lB, OT = 0, LT = 0;
+#pragma unroll
+    for (uint32_t ww = 0; ww < kBW; ++ww) {
+      const uint4 t = lds128(tab + ww * 16);
+      bv.og[ww] = oB + OT;
+      if (ww == w) { og = oB + OT; lg = lB + LT; }
+      OT += t.x;
+      LT += t.y;
+    }
+    const uint32_t op = og + (ex >> 16), lp = lg + (ex & 0xffffu), dst = op + lit, src = dst - dist;
+    const bool has = act && L;
+    const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst);
+    const bool bad_rec = act && !mcode && (r >> 16);
+    const bool bad_sz = og + out_sum > ulen || lg + lit_sum > e.n_lit;
+    const bool any_rec = __any_sync(FULL, bad_rec), any_ref = __any_sync(FULL, bad_ref);
+    const bool de_ok = __all_sync(FULL, !has || src + L <= og || src >= op);
+    const bool fast_g = de_ok && (og & 3u) + out_sum <= kGrpMaxOut && lit_sum + 16 <= kLbuf;
+    if (lane == 0) {
+      if (any_ref || any_rec || bad_sz)
+        report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
+      sts32(flg + w * 4, ((any_ref || any_rec || bad_sz) ? 1u : 0u) | (fast_g ? 0u : 2u) | (de_ok ? 0u : 4u));
+    }
+    __syncthreads();
+    uint32_t fl = 0;
+#pragma unroll
+    for (uint32_t ww = 0; ww < kBW; ++ww) fl |= lds32(flg + ww * 4);
+    if (fl & 1u) return;                                       // device error already reported
+    const bool batch_fast = !(fl & 2u) && OT + a.window + 16 <= RING && oB + OT - flushed <= RING;
+    if (batch_fast) {
+      // stage this group's literal bytes [lg, lg + lit_sum) (16-byte chunks) into its literal buffer
+      const uint8_t* la = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits + lg) & ~uintptr_t(15));
+      const uint32_t lofs = uint32_t((lits + lg) - la), nch = (lofs + lit_sum + 15) / 16;
+      for (uint32_t c = lane; c < nch; c += 32) cp_async16(lbuf_s + 16 * c, la + 16 * c);
+      cp_commit();
+      // descriptors: start, literal end | own << 31, literal delta, match delta (own: lbuf, else distance)
+      const uint32_t opr = ex >> 16, ob = og & 3u;
+      const uint32_t ldl = lofs + (ex & 0xffffu) - opr;
+      const bool own = has && src >= op;
+      sts128(prm_s + lane * 16, make_uint4(act ? opr : out_sum, (opr + lit) | (own ? 0x80000000u : 0u), ldl,
+                                           own ? ldl - dist : dist));
+      if (act) ats_or(bits_s + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
+      __syncwarp();
+      // exclusive prefix counts of the bitmap words (lane l: words 4l .. 4l+3)
+      {
+        const uint4 bw = lds128(bits_s + lane * 16);
+        const uint32_t c0 = __popc(bw.x), c1 = __popc(bw.y), c2 = __popc(bw.z), c3 = __popc(bw.w);
+        const uint32_t s4 = c0 + c1 + c2 + c3;
+        const uint32_t ex4 = warp_incl_scan_u32(s4, lane) - s4;
+        sts128(pcnt_s + lane * 16, make_uint4(ex4, ex4 + c0, ex4 + c0 + c1, ex4 + c0 + c1 + c2));
+      }
+      cp_wait_n<0>();
+      __syncthreads();
+      // a6 + a7: byte rows of this group (rows aligned to the bitmap words: y = x + ob)
+      const uint32_t nrows = (ob + out_sum + 31) / 32;
+      const uint32_t le = (2u << lane) - 1u;
+      for (uint32_t r0 = 0; r0 < nrows; r0 += 4) {
+        uint32_t byte[4];
+#pragma unroll
+        for (uint32_t rr = 0; rr < 4; ++rr) {
+          const uint32_t row = r0 + rr;
+          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
+          byte[rr] = 0;
+          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) {
+            const uint32_t bw = lds32(bits_s + row * 4), pc = lds32(pcnt_s + row * 4);
+            const uint32_t j = pc + __popc(bw & le) - 1u;
+            const uint4 D = lds128(prm_s + j * 16);
+            const uint32_t xu = uint32_t(x);
+            if (xu < (D.y & 0x7fffffffu)) byte[rr] = lds8(lbuf_s + xu + D.z);
+            else if (D.y >> 31) byte[rr] = lds8(lbuf_s + xu + D.w);
+            else {
+              const uint32_t q = og + xu - D.w;
+              byte[rr] = q < oB ? lds8(ring + (q & RM)) : chase_byte(bv, q);
+            }
+          }
+        }
+#pragma unroll
+        for (uint32_t rr = 0; rr < 4; ++rr) {
+          const uint32_t row = r0 + rr;
+          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
+          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) sts8(ring + ((og + uint32_t(x)) & RM), byte[rr]);
+        }
+      }
+      if (STATS) {
+        const uint32_t any = __ballot_sync(FULL, has);
+        uint32_t bytes = has ? L : 0u;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
+        if (lane == 0 && g < ngroups) {
+          atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
+          if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
+        }
+      }
+      __syncthreads();
+      sts128(bits_s + lane * 16, make_uint4(0u, 0u, 0u, 0u));
+      // flush completed 16-byte chunks (all warps), at least kFlushBytes at a time
+      const uint32_t q1 = (oB + OT) >> 4;
+      if (q1 * 16 >= flushed + kFlushBytes) {
+        for (uint32_t q = (flushed >> 4) + threadIdx.x; q < q1; q += 32 * kBW)
+          reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
+        flushed = q1 * 16;
+      }
+    } else {
+      // slow batch (a group too large for the buffers, or not DE): flush the ring, then warp 0 runs the groups
+      // of the batch one by one in global memory with MRR (exact for any valid file), then reload the window
+      for (uint32_t p = flushed + threadIdx.x; p < oB; p += 32 * kBW) out[p] = uint8_t(lds8(ring + (p & RM)));
+      __syncthreads();
+      if (w == 0) {
+        for (uint32_t ww = 0; ww < kBW; ++ww) {
+          const uint32_t gg = B0 + ww, ii = gg * 32 + lane;
+          if (gg >= ngroups) break;
+          if (STATS && lane == 0 && (lds32(flg + ww * 4) & 4u)) atomicAdd(stats_ptr(a) + 66, 1ull);
+          const bool act2 = ii < n_seq;
+          const uint32_t r2 = act2 ? __ldg(recs + ii) : 0u;
+          const uint32_t lit2 = r2 & 1023u, mc2 = (r2 >> 10) & 63u, dist2 = (r2 >> 16) + 1u;
+          const uint32_t L2 = mc2 ? mc2 + mm1 : 0u, v2 = lit2 | ((lit2 + L2) << 16);
+          const uint32_t inc2 = warp_incl_scan_u32(v2, lane), ex2 = inc2 - v2;
+          const uint32_t op2 = bv.og[ww] + (ex2 >> 16);
+          uint32_t lg2 = lB;
+          for (uint32_t u = 0; u < ww; ++u) lg2 += lds128(tab + u * 16).y;
+          const uint32_t lp2 = lg2 + (ex2 & 0xffffu), dst2 = op2 + lit2;
+          if (act2) copy_lits_global(out + op2, lits + lp2, lit2);
+          if (!resolve_group<GOMP_STRAT_MRR, STATS>(a, go, lane, act2 && L2, dst2, dst2 - dist2, L2, op2, b, gg * 32))
+            break;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      const uint32_t o_new = oB + OT;
+      const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
+      for (uint32_t p = o_new - keep + threadIdx.x; p < o_new; p += 32 * kBW) sts8(ring + (p & RM), out[p]);
+      flushed = o_new;
+      __syncthreads();
+    }
+    oB += OT;
+    lB += LT;
+  }
+  __syncthreads();
+  if (oB != ulen || lB != e.n_lit) {
+    if (threadIdx.x == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
+    return;
+  }
+  const uint32_t q1 = oB >> 4;
+  for (uint32_t q = (flushed >> 4) + threadIdx.x; q < q1; q += 32 * kBW)
+    reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
+  for (uint32_t p = max(q1 * 16, flushed) + threadIdx.x; p < oB; p += 32 * kBW) out[p] = uint8_t(lds8(ring + (p & RM)));
+}
+
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
   const dim3 grid((a.n_blocks + kLz77Warps - 1) / kLz77Warps), block(32 * kLz77Warps);
@@ -1158,7 +1402,17 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
   }
   switch (s) {
-    case GOMP_STRAT_DE: launch_lz77<GOMP_STRAT_DE>(a, stats, byte_mode, st); break;
+    case GOMP_STRAT_DE: {
+      const size_t smem = lzb_smem_bytes(a.ring_bytes);
+      if (stats) {
+        cudaFuncSetAttribute(lz77_batch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        lz77_batch_kernel<true><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
+      } else {
+        cudaFuncSetAttribute(lz77_batch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        lz77_batch_kernel<false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
+      }
+      break;
+    }
     case GOMP_STRAT_MRR: launch_lz77<GOMP_STRAT_MRR>(a, stats, byte_mode, st); break;
     default: launch_lz77<GOMP_STRAT_SC>(a, stats, byte_mode, st); break;
   }
