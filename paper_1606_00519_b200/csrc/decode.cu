@@ -1230,8 +1230,12 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       __syncthreads();
       // a6 + a7: aligned output words of this group, lane t -> words t, t+32, ... (y = x + ob)
       const uint32_t nwords = (ob + out_sum + 3) >> 2, wbase = og >> 2;
+      const int32_t bend = int32_t(oB + OT - og);                      // batch end, group-relative
       for (uint32_t k = lane; k < nwords; k += 32) {
         const int32_t x0 = int32_t(4 * k) - int32_t(ob);
+        // a word is written by the group holding its first byte (the batch's first group also writes its
+        // leading shared word, keeping the bytes of the previous, complete batch)
+        if (x0 < 0 && w > 0) continue;
         const uint32_t yy = x0 < 0 ? ob : 4 * k;                       // first byte of the word inside the group
         const uint32_t wi = yy >> 5, bb = yy & 31;
         const uint32_t bw = lds32(bits_s + wi * 4);
@@ -1276,6 +1280,9 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
             ++sg;
             if (cs < xe) D = lds64(prm_s + sg * 8);
           }
+          // bytes of the next group of this batch that share the word: resolved by chasing (no race)
+          for (int32_t xb = xe; xb < min(x0 + 4, bend); ++xb)
+            val = (val & ~(0xffu << (8 * (xb - x0)))) | (chase_byte(bv, og + uint32_t(xb)) << (8 * (xb - x0)));
         }
         sts32(ring + ((4 * (wbase + k)) & RM), val);
       }
