@@ -170,12 +170,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ uint2 lds64(uint32_t a) {
-  uint2 v; asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory"); return v;
-}
-__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
-}
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
@@ -1092,26 +1086,22 @@ struct BatchView {
   uint32_t og[kBW];
 };
 
-// value of output byte q (absolute in the block) of the current batch: chase through earlier groups' segment
-// tables until the source lies below the batch start (final in the ring) or in a literal buffer
+// value of output byte q (absolute in the block) of the current batch: chase through earlier groups
 __device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
 #pragma unroll 1
   for (uint32_t hop = 0; hop < kBW; ++hop) {
     if (q < v.oB) return lds8(v.ring + (q & v.RM));
-    uint32_t h = 0, oh = v.og[0];
+    uint32_t h = 0;
 #pragma unroll
-    for (uint32_t hh = 1; hh < kBW; ++hh) {
-      const bool in = v.og[hh] <= q;
-      h = in ? hh : h;
-      oh = in ? v.og[hh] : oh;
-    }
+    for (uint32_t hh = 1; hh < kBW; ++hh) h = v.og[hh] <= q ? hh : h;
     const uint32_t hs = v.slot0 + h * kSlot;
-    const uint32_t xr = q - oh, y = xr + (oh & 3u);
+    const uint32_t xr = q - v.og[h], y = xr + (v.og[h] & 3u);
     const uint32_t bw = lds32(hs + 512 + (y >> 5) * 4), pc = lds32(hs + 512 + kGrpBitWords * 4 + (y >> 5) * 4);
     const uint32_t j = pc + __popc(bw & ((2u << (y & 31)) - 1u)) - 1u;
-    const uint2 D = lds64(hs + j * 8);
-    if (!(D.x >> 31)) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.y);
-    q = xr + D.y;
+    const uint4 D = lds128(hs + j * 16);
+    if (xr < (D.y & 0x7fffffffu)) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.z);
+    if (D.y >> 31) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.w);
+    q -= D.w;
   }
   return lds8(v.ring + (q & v.RM));
 }
@@ -1203,20 +1193,13 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       const uint32_t lofs = uint32_t((lits + lg) - la), nch = (lofs + lit_sum + 15) / 16;
       for (uint32_t c = lane; c < nch; c += 32) cp_async16(lbuf_s + 16 * c, la + 16 * c);
       cp_commit();
-      // segment table: every non-empty literal string and back-reference of the group is one segment
-      // {start | ring << 31, delta}: byte x of it is lbuf[x + delta], or output byte x + delta (absolute)
+      // descriptors: start, literal end | own << 31, literal delta, match delta (own: lbuf, else distance)
       const uint32_t opr = ex >> 16, ob = og & 3u;
       const uint32_t ldl = lofs + (ex & 0xffffu) - opr;
       const bool own = has && src >= op;
-      const bool sl = act && lit > 0, sm_ = has;
-      const uint32_t nsg = (sl ? 1u : 0u) + (sm_ ? 1u : 0u);
-      const uint32_t sinc = warp_incl_scan_u32(nsg, lane), sidx = sinc - nsg;
-      const uint32_t nseg = __shfl_sync(FULL, sinc, 31);
-      if (sl) sts64(prm_s + sidx * 8, opr, ldl);
-      if (sm_) sts64(prm_s + (sidx + (sl ? 1u : 0u)) * 8, (opr + lit) | (own ? 0u : 0x80000000u),
-                     own ? ldl - dist : og - dist);
-      if (sl) ats_or(bits_s + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
-      if (sm_) ats_or(bits_s + ((opr + lit + ob) >> 5) * 4, 1u << ((opr + lit + ob) & 31));
+      sts128(prm_s + lane * 16, make_uint4(act ? opr : out_sum, (opr + lit) | (own ? 0x80000000u : 0u), ldl,
+                                           own ? ldl - dist : dist));
+      if (act) ats_or(bits_s + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
       __syncwarp();
       // exclusive prefix counts of the bitmap words (lane l: words 4l .. 4l+3)
       {
@@ -1228,63 +1211,35 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       }
       cp_wait_n<0>();
       __syncthreads();
-      // a6 + a7: aligned output words of this group, lane t -> words t, t+32, ... (y = x + ob)
-      const uint32_t nwords = (ob + out_sum + 3) >> 2, wbase = og >> 2;
-      const int32_t bend = int32_t(oB + OT - og);                      // batch end, group-relative
-      for (uint32_t k = lane; k < nwords; k += 32) {
-        const int32_t x0 = int32_t(4 * k) - int32_t(ob);
-        // a word is written by the group holding its first byte (the batch's first group also writes its
-        // leading shared word, keeping the bytes of the previous, complete batch)
-        if (x0 < 0 && w > 0) continue;
-        const uint32_t yy = x0 < 0 ? ob : 4 * k;                       // first byte of the word inside the group
-        const uint32_t wi = yy >> 5, bb = yy & 31;
-        const uint32_t bw = lds32(bits_s + wi * 4);
-        uint32_t sg = lds32(pcnt_s + wi * 4) + __popc(bw & ((2u << bb) - 1u)) - 1u;
-        const uint32_t inner = (bw >> bb) >> 1 & ((1u << (4 * k + 3 - yy)) - 1u);   // starts inside the word
-        uint2 D = lds64(prm_s + sg * 8);
-        uint32_t val;
-        if (x0 >= 0 && inner == 0 && uint32_t(x0) + 4 <= out_sum) {
-          const uint32_t pp = uint32_t(x0) + D.y;
-          if (D.x >> 31) {
-            val = pp + 3 < oB ? ring_word_at(ring, RM, pp) : 0u;
-            if (pp + 3 >= oB) {
+      // a6 + a7: byte rows of this group (rows aligned to the bitmap words: y = x + ob)
+      const uint32_t nrows = (ob + out_sum + 31) / 32;
+      const uint32_t le = (2u << lane) - 1u;
+      for (uint32_t r0 = 0; r0 < nrows; r0 += 4) {
+        uint32_t byte[4];
 #pragma unroll
-              for (uint32_t t = 0; t < 4; ++t) val |= chase_byte(bv, pp + t) << (8 * t);
+        for (uint32_t rr = 0; rr < 4; ++rr) {
+          const uint32_t row = r0 + rr;
+          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
+          byte[rr] = 0;
+          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) {
+            const uint32_t bw = lds32(bits_s + row * 4), pc = lds32(pcnt_s + row * 4);
+            const uint32_t j = pc + __popc(bw & le) - 1u;
+            const uint4 D = lds128(prm_s + j * 16);
+            const uint32_t xu = uint32_t(x);
+            if (xu < (D.y & 0x7fffffffu)) byte[rr] = lds8(lbuf_s + xu + D.z);
+            else if (D.y >> 31) byte[rr] = lds8(lbuf_s + xu + D.w);
+            else {
+              const uint32_t q = og + xu - D.w;
+              byte[rr] = q < oB ? lds8(ring + (q & RM)) : chase_byte(bv, q);
             }
-          } else {
-            val = ring_word_at(lbuf_s, kLbuf - 1, pp);
           }
-        } else {
-          val = x0 < 0 ? lds32(ring + ((4 * (wbase + k)) & RM)) : 0u;
-          const int32_t xs = x0 < 0 ? 0 : x0, xe = min(x0 + 4, int32_t(out_sum));
-          int32_t cs = xs;
-#pragma unroll 1
-          while (cs < xe) {
-            const uint32_t nxt = sg + 1 < nseg ? (lds64(prm_s + (sg + 1) * 8).x & 0x7fffffffu) : out_sum;
-            const int32_t ce = min(int32_t(nxt), xe);
-            const uint32_t m = byte_mask(cs - x0, ce - x0);
-            const uint32_t pp = uint32_t(x0) + D.y;
-            uint32_t vv = 0;
-            if (D.x >> 31) {
-              if (pp + 3 < oB) vv = ring_word_at(ring, RM, pp);
-              else {
-#pragma unroll
-                for (uint32_t t = 0; t < 4; ++t)
-                  if ((m >> (8 * t)) & 1u) vv |= chase_byte(bv, pp + t) << (8 * t);
-              }
-            } else {
-              vv = ring_word_at(lbuf_s, kLbuf - 1, pp);
-            }
-            val = (val & ~m) | (vv & m);
-            cs = ce;
-            ++sg;
-            if (cs < xe) D = lds64(prm_s + sg * 8);
-          }
-          // bytes of the next group of this batch that share the word: resolved by chasing (no race)
-          for (int32_t xb = xe; xb < min(x0 + 4, bend); ++xb)
-            val = (val & ~(0xffu << (8 * (xb - x0)))) | (chase_byte(bv, og + uint32_t(xb)) << (8 * (xb - x0)));
         }
-        sts32(ring + ((4 * (wbase + k)) & RM), val);
+#pragma unroll
+        for (uint32_t rr = 0; rr < 4; ++rr) {
+          const uint32_t row = r0 + rr;
+          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
+          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) sts8(ring + ((og + uint32_t(x)) & RM), byte[rr]);
+        }
       }
       if (STATS) {
         const uint32_t any = __ballot_sync(FULL, has);
