@@ -685,21 +685,34 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
         }
         const uint32_t lits0 = on ? (lds32(recs_s + (merged * 32 + lane) * 4) >> 16) & 0xffu : 0u;
         const uint32_t nlen0 = on ? lds32(recs_s + (merged * 32 + lane) * 4) >> 24 : 0u;
+#ifdef GOMP_FORCE_PASS2
+        const bool ovf = true;
+#else
         const bool ovf = __any_sync(FULL, on && (lits > cap || nlen > cap));
+#endif
+#ifdef GOMP_DEBUG_SPEC
+        if (bi == 0 && k == 1) {
+          uint32_t* dbg = reinterpret_cast<uint32_t*>(a.dst) + lane * 16;
+          dbg[0] = on; dbg[1] = merged; dbg[2] = nlen0; dbg[3] = nlen; dbg[4] = lits0; dbg[5] = lits;
+          dbg[6] = t_start; dbg[7] = e_pos; dbg[8] = exit_lane; dbg[9] = exit_idx; dbg[10] = seq_inc - seqs;
+          dbg[11] = n_it; dbg[12] = lead_t; dbg[13] = runin; dbg[14] = cap; dbg[15] = c;
+        }
+#endif
         if (!ovf) {
           // ---------------- compaction: the true segment's records/literals from scratch to their final place
           const uint32_t fin = has_t ? trail_t : runin + lits_t;     // pending literal run at the lane's exit
           const bool eob_ok = (last && is_tail) ? (eob_it == n_it) : (eob_it <= merged);
           if (on && (bad_it > merged || !eob_ok)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
           uint32_t* rp = rec + (seq_inc - seqs);
-          for (uint32_t r = nlen0; r < nlen; ++r) {
+          const uint32_t nlen_end = on ? nlen : nlen0, lits_end = on ? lits : lits0;   // off-chain lanes own nothing
+          for (uint32_t r = nlen0; r < nlen_end; ++r) {
             uint32_t v = srec[r];
             if (r == nlen0) v = (v & ~1023u) | (runin + lead_t);   // the run entering the true segment
             rp[r - nlen0] = v;
           }
           if (last && is_tail && fin != 0) rp[nlen_t] = fin;           // EOB-closed literal-only sequence
           uint8_t* lq = lit + (lit_inc - lits_t);
-          for (uint32_t r = lits0; r < lits; ++r) lq[r - lits0] = slit[r];
+          for (uint32_t r = lits0; r < lits_end; ++r) lq[r - lits0] = slit[r];
           continue;
         }
         // ---------------- pass 2 (scratch overflow): decode again from the true start, writing directly
