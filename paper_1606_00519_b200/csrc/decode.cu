@@ -39,8 +39,6 @@ struct Args {
   uint64_t total, file_len, payload_base, tok_stride;
   uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, lut_bits, max_tok;
   uint32_t n_sub_total, nb_total, ring_bytes;
-  uint8_t* scratch;       // Bit, warp decoder: per (persistent CTA, warp, lane) record + literal scratch
-  uint32_t scr_cap;       // entries per lane (records and literals each)
 };
 
 // ------------------------------------------------------------------ completion: error word (a9)
@@ -491,11 +489,12 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
 // makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
 constexpr uint32_t kRec = 32;            // recorded iteration boundaries per lane (self-sync window)
 constexpr uint32_t kSpecRing = 4;        // 16-byte chunks per lane bit ring
+constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this use one lane (serial)
 
 __host__ __device__ constexpr uint32_t spec_warp_bytes() { return 32 * (kSpecRing * 16 + kRec * 4); }
 
 template <bool LONG>
-__global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
+__global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
@@ -506,24 +505,16 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
   const uint32_t ring_s = wbase_s + lane * (kSpecRing * 16);           // this lane's bit ring
   // [kRec][32] recorded boundaries: (position - lane start) | literals before it << 16 | length codes << 24
   const uint32_t recs_s = wbase_s + 32 * kSpecRing * 16;
-  // this lane's scratch (persistent CTA slot = blockIdx.x): records then literals, scr_cap entries each
-  const uint64_t lane_id = (uint64_t(blockIdx.x) * nwarps + warp) * 32 + lane;
-  uint32_t* const srec = reinterpret_cast<uint32_t*>(a.scratch) + lane_id * a.scr_cap;
-  uint8_t* const slit = a.scratch + uint64_t(gridDim.x) * nwarps * 32 * a.scr_cap * 4 + lane_id * a.scr_cap;
-  const uint32_t cap = a.scr_cap;
-  // persistent CTAs: block bi, bi + gridDim.x, ... of the launched range
-  for (uint32_t bi = blockIdx.x; bi < a.n_blocks; bi += gridDim.x) {
-  const uint32_t b = a.first_block + bi;
-  __syncthreads();                                   // the previous block's tables are no longer in use
+  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
   if (!huff_block_ok(a, e, block_ulen(a, b))) {
     if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
-    continue;
+    return;
   }
   const uint8_t* pl = a.src + e.payload_off;
   if (!build_tables<LONG>(sm, lut_ll, lut_d, pl, a)) {
     if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
-    continue;
+    return;
   }
   const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
   const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
@@ -535,6 +526,7 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
   const uint8_t* gbits = pl + kTreeBytes;
+  const uint32_t le = (2u << lane) - 1u, lt = (1u << lane) - 1u;
 
   for (uint32_t k = warp; k < e.n_sub; k += nwarps) {
     // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
@@ -565,20 +557,11 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
       const uint32_t endb = S0 + bsz;
       uint32_t lits = 0, nlen = 0, lead = 0, run = 0, first_len_seen = 0;
       uint32_t lead_after_rec = 0xffffffffu;   // literals before the first length code at iteration >= kRec-1
-      uint32_t bad_it = 0, eob_it = 0, n_it = 0;  // 1 + last iteration with an invalid symbol / EOB; iterations
       BitRing<kSpecRing> in;
       in.init(ring_s, gbits, gmax, sp);
-      // every iteration also writes its record / literal to this lane's scratch (validated and compacted once
-      // the true path is known, so the sub-block is decoded only once)
       auto account = [&](const Step& st, uint32_t it) {
-        in.consume(st.kind == K_BAD ? 1u : 0u);   // garbage before self-synchronisation
+        in.consume(st.kind == K_BAD ? 1u : 0u);   // garbage before self-synchronisation (validated in pass 2)
         const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
-        if (islit && lits < cap) slit[lits] = uint8_t(st.byte);
-        if (isl && nlen < cap) srec[nlen] = run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16);
-        const bool badsym = st.bad || st.kind == K_BAD || (isl && (st.L < a.min_match || st.L > a.max_match));
-        bad_it = badsym ? it + 1 : bad_it;
-        eob_it = st.kind == K_EOB ? it + 1 : eob_it;
-        n_it = it + 1;
         lits += islit ? 1u : 0u;
         run += islit ? 1u : 0u;
         lead = (isl && !first_len_seen) ? lits : lead;
@@ -683,39 +666,7 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
           if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 9u);
           continue;
         }
-        const uint32_t lits0 = on ? (lds32(recs_s + (merged * 32 + lane) * 4) >> 16) & 0xffu : 0u;
-        const uint32_t nlen0 = on ? lds32(recs_s + (merged * 32 + lane) * 4) >> 24 : 0u;
-#ifdef GOMP_FORCE_PASS2
-        const bool ovf = true;
-#else
-        const bool ovf = __any_sync(FULL, on && (lits > cap || nlen > cap));
-#endif
-#ifdef GOMP_DEBUG_SPEC
-        if (bi == 0 && k == 1) {
-          uint32_t* dbg = reinterpret_cast<uint32_t*>(a.dst) + lane * 16;
-          dbg[0] = on; dbg[1] = merged; dbg[2] = nlen0; dbg[3] = nlen; dbg[4] = lits0; dbg[5] = lits;
-          dbg[6] = t_start; dbg[7] = e_pos; dbg[8] = exit_lane; dbg[9] = exit_idx; dbg[10] = seq_inc - seqs;
-          dbg[11] = n_it; dbg[12] = lead_t; dbg[13] = runin; dbg[14] = cap; dbg[15] = c;
-        }
-#endif
-        if (!ovf) {
-          // ---------------- compaction: the true segment's records/literals from scratch to their final place
-          const uint32_t fin = has_t ? trail_t : runin + lits_t;     // pending literal run at the lane's exit
-          const bool eob_ok = (last && is_tail) ? (eob_it == n_it) : (eob_it <= merged);
-          if (on && (bad_it > merged || !eob_ok)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
-          uint32_t* rp = rec + (seq_inc - seqs);
-          const uint32_t nlen_end = on ? nlen : nlen0, lits_end = on ? lits : lits0;   // off-chain lanes own nothing
-          for (uint32_t r = nlen0; r < nlen_end; ++r) {
-            uint32_t v = srec[r];
-            if (r == nlen0) v = (v & ~1023u) | (runin + lead_t);   // the run entering the true segment
-            rp[r - nlen0] = v;
-          }
-          if (last && is_tail && fin != 0) rp[nlen_t] = fin;           // EOB-closed literal-only sequence
-          uint8_t* lq = lit + (lit_inc - lits_t);
-          for (uint32_t r = lits0; r < lits_end; ++r) lq[r - lits0] = slit[r];
-          continue;
-        }
-        // ---------------- pass 2 (scratch overflow): decode again from the true start, writing directly
+        // ---------------- pass 2: decode from the true start, write records and literals
         uint32_t run = runin, bad = 0;
         uint32_t* rp = rec + (seq_inc - seqs);
         uint32_t* const rend = rec + nseq;
@@ -755,7 +706,6 @@ __global__ void __launch_bounds__(512, 2) huff_warp_kernel(const Args a) {
     }
     __syncwarp();
   }
-  }   // persistent block loop
 }
 
 // ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
@@ -1421,31 +1371,32 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   while (a.ring_bytes < info->window_size + 4096) a.ring_bytes <<= 1;
   const bool byte_mode = info->mode == GOMP_MODE_BYTE;
   if (!byte_mode && !lz77_only) {
-    const HuffPlan hp = huff_plan(*info, nblk);
+    const uint64_t nb = std::max<uint32_t>(info->n_blocks, 1);
+    const uint64_t avg_sub = (uint64_t(info->n_sub_total) + nb - 1) / nb;
+    const uint64_t avg_bits = info->n_sub_total ? (info->file_len - info->payload_base) * 8 / info->n_sub_total : 0;
     const bool LONGc = info->cwl > a.lut_bits;
     const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << a.lut_bits) * sizeof(uint32_t);
-    a.scratch = a.tokens + align256(uint64_t(nblk) * a.tok_stride + 64);
-    a.scr_cap = hp.cap;
-    if (hp.warp) {
-      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode,
-      // persistent CTAs (2 per SM) over the blocks
-      const size_t smem = tabs + size_t(hp.nw) * spec_warp_bytes();
+    if (avg_bits >= 4 * kSpecMinBits) {
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode
+      const uint32_t nw = uint32_t(std::min<uint64_t>(16, std::max<uint64_t>(1, avg_sub)));
+      const size_t smem = tabs + size_t(nw) * spec_warp_bytes();
       if (LONGc) {
         cudaFuncSetAttribute(huff_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<true><<<hp.ctas, 32 * hp.nw, smem, st>>>(a);
+        huff_warp_kernel<true><<<nblk, 32 * nw, smem, st>>>(a);
       } else {
         cudaFuncSetAttribute(huff_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<false><<<hp.ctas, 32 * hp.nw, smem, st>>>(a);
+        huff_warp_kernel<false><<<nblk, 32 * nw, smem, st>>>(a);
       }
     } else {
       // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block
-      const size_t smem = tabs + size_t(hp.nw) * 128;
+      const uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
+      const size_t smem = tabs + size_t(nt) * 128;
       if (LONGc) {
         cudaFuncSetAttribute(huff_thread_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_thread_kernel<true><<<nblk, hp.nw, smem, st>>>(a);
+        huff_thread_kernel<true><<<nblk, nt, smem, st>>>(a);
       } else {
         cudaFuncSetAttribute(huff_thread_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_thread_kernel<false><<<nblk, hp.nw, smem, st>>>(a);
+        huff_thread_kernel<false><<<nblk, nt, smem, st>>>(a);
       }
     }
     if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;

@@ -18,37 +18,6 @@ constexpr uint32_t kMaxLitRun = 1023;  // reading R10
 constexpr size_t kWsHeaderBytes = 1024;  // workspace: error word + stats, then the token buffer
 
 inline uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
-inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
-
-// Launch plan of the Bit decoder, shared by the workspace sizing (api.cpp) and the launcher (decode.cu).
-constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this are decoded by one lane
-constexpr uint32_t kHuffCtas = 296;         // persistent CTAs of the warp decoder (2 per SM on 148 SMs)
-struct HuffPlan {
-  bool warp;          // warp-per-sub-block speculative decoder (else thread per sub-block)
-  uint32_t nw;        // warps per CTA (warp decoder) / threads per CTA (thread decoder)
-  uint32_t ctas;      // grid
-  uint32_t cap;       // scratch entries per lane
-  uint64_t scratch;   // scratch bytes
-};
-inline HuffPlan huff_plan(const gomp_info& in, uint32_t nblk) {
-  HuffPlan p{};
-  const uint64_t nb = in.n_blocks ? in.n_blocks : 1;
-  const uint64_t avg_sub = (uint64_t(in.n_sub_total) + nb - 1) / nb;
-  const uint64_t avg_bits = in.n_sub_total ? (in.file_len - in.payload_base) * 8 / in.n_sub_total : 0;
-  p.warp = avg_bits >= 4 * kSpecMinBits;
-  if (p.warp) {
-    p.nw = uint32_t(avg_sub < 16 ? (avg_sub ? avg_sub : 1) : 16);
-    p.ctas = nblk < kHuffCtas ? nblk : kHuffCtas;
-    const uint64_t c = avg_bits / 32;
-    p.cap = uint32_t(c / 6 + 64 < 4096 ? c / 6 + 64 : 4096);
-    p.scratch = uint64_t(p.ctas) * p.nw * 32 * p.cap * 5;
-  } else {
-    const uint64_t nt = (avg_sub + 31) / 32 * 32;
-    p.nw = uint32_t(nt < 32 ? 32 : nt > 256 ? 256 : nt);
-    p.ctas = nblk;
-  }
-  return p;
-}
 inline uint32_t ld32(const uint8_t* p) { uint32_t v; std::memcpy(&v, p, 4); return v; }
 inline uint64_t ld64(const uint8_t* p) { uint64_t v; std::memcpy(&v, p, 8); return v; }
 inline void st32(uint8_t* p, uint32_t v) { std::memcpy(p, &v, 4); }
