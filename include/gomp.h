@@ -59,6 +59,10 @@ typedef enum {
  * DECODE_ONLY call left in the same workspace. Ignored for Byte files (single fused kernel). */
 #define GOMP_FLAG_DECODE_ONLY 0x200
 #define GOMP_FLAG_LZ77_ONLY 0x400
+/* Testing only: force the Bit decoder variant (default: chosen from the mean sub-block size). HUFF_THREAD =
+ * one thread per sub-block (the paper's scheme); HUFF_WARP = one warp per sub-block, speculative. */
+#define GOMP_FLAG_HUFF_THREAD 0x800
+#define GOMP_FLAG_HUFF_WARP 0x1000
 
 /* Compression parameters. Defaults (gomp_params_default) = the paper's setup. */
 typedef struct {

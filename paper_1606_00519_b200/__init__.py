@@ -21,6 +21,8 @@ STRATEGIES = {"auto": 0, "de": 1, "mrr": 2, "sc": 3}
 FLAG_STATS = 0x100
 FLAG_DECODE_ONLY = 0x200
 FLAG_LZ77_ONLY = 0x400
+FLAG_HUFF_THREAD = 0x800
+FLAG_HUFF_WARP = 0x1000
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_MAGIC", -3: "UNSUPPORTED_VERSION", -4: "TRUNCATED",
           -5: "HEADER_INCONSISTENT", -6: "CORRUPT_STREAM", -7: "MALFORMED_BACKREF", -8: "NO_PROGRESS",
           -9: "DST_TOO_SMALL", -10: "WORKSPACE_TOO_SMALL", -11: "CUDA", -12: "OOM"}
@@ -181,17 +183,19 @@ def _stream_ptr(stream, device):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _strategy(strategy, stats, phase=None):
+def _strategy(strategy, stats, phase=None, huff=None):
     s = STRATEGIES[strategy] if isinstance(strategy, str) else int(strategy)
     s |= {None: 0, "decode": FLAG_DECODE_ONLY, "lz77": FLAG_LZ77_ONLY}[phase]
+    s |= {None: 0, "thread": FLAG_HUFF_THREAD, "warp": FLAG_HUFF_WARP}[huff]
     return s | (FLAG_STATS if stats else 0)
 
 
 def decompress_into(info, src, dst, workspace, strategy="auto", stream=None, first_block=0, n_blocks=None,
-                    stats=False, phase=None):
+                    stats=False, phase=None, huff=None):
     """Enqueue gomp_decompress(_blocks) on `stream` (no synchronisation). src/dst/workspace: CUDA uint8
     tensors; dst receives block first_block at dst[0]. phase="decode"/"lz77" runs one kernel of a Bit
-    decompression (profiling only, GOMP_FLAG_DECODE_ONLY / GOMP_FLAG_LZ77_ONLY)."""
+    decompression (profiling only, GOMP_FLAG_DECODE_ONLY / GOMP_FLAG_LZ77_ONLY); huff="thread"/"warp"
+    forces the Bit decoder variant (testing, GOMP_FLAG_HUFF_THREAD / GOMP_FLAG_HUFF_WARP)."""
     for t in (src, dst, workspace):
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8 and t.is_contiguous()):
             raise ValueError("decompress_into needs contiguous CUDA uint8 tensors (no CPU fallback)")
@@ -199,7 +203,7 @@ def decompress_into(info, src, dst, workspace, strategy="auto", stream=None, fir
     nb = info.n_blocks - first_block if n_blocks is None else n_blocks
     _check(lib().gomp_decompress_blocks(ctypes.byref(info), first_block, nb, src.data_ptr(), src.numel(),
                                         dst.data_ptr(), dst.numel(), workspace.data_ptr(), workspace.numel(),
-                                        _strategy(strategy, stats, phase), sp), "gomp_decompress")
+                                        _strategy(strategy, stats, phase, huff), sp), "gomp_decompress")
 
 
 def read_error(workspace, stream=None):
@@ -216,7 +220,8 @@ def read_stats(workspace, stream=None):
     return {"rounds": list(s.rounds), "bytes": list(s.bytes), "de_fallback_groups": s.de_fallback_groups}
 
 
-def decompress(c, out=None, strategy="auto", stream=None, info=None, check=True, stats=False, return_stats=False):
+def decompress(c, out=None, strategy="auto", stream=None, info=None, check=True, stats=False, return_stats=False,
+               huff=None):
     """Decompress a Gompresso file held in a CUDA uint8 tensor; returns a CUDA uint8 tensor.
     check=True synchronises and raises GompError on a device-detected error."""
     if not (isinstance(c, torch.Tensor) and c.is_cuda):
@@ -225,7 +230,7 @@ def decompress(c, out=None, strategy="auto", stream=None, info=None, check=True,
     if out is None:
         out = torch.empty(max(info.uncompressed_len, 1), dtype=torch.uint8, device=c.device)
     ws = torch.empty(workspace_size(info), dtype=torch.uint8, device=c.device)
-    decompress_into(info, c, out, ws, strategy, stream, stats=stats or return_stats)
+    decompress_into(info, c, out, ws, strategy, stream, stats=stats or return_stats, huff=huff)
     if check:
         e = read_error(ws, stream)
         if e.status:

@@ -89,21 +89,27 @@ __constant__ uint16_t c_dist_base[30] = {1,    2,    3,    4,    5,    7,    9, 
 __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6,
                                          6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 
-// LUT entry: bits 0-3 code length (0 = not resolvable by the table: long code or invalid), 4-5 kind,
-// litlen: literal byte or length base in bits 8-16, extra-bit count in 17-19; dist: base 8-23, extra 24-27.
+// LUT entries (32 bits). litlen E: bits 0-4 bits spanned (code + extra; 0 = not resolvable by the table: a
+// long code), 5-8 code length, 9-10 kind, 11-13 extra-bit count, 16-24 literal byte or length base.
+// distance D: 0-4 bits spanned, 5-8 code length, 9-12 extra-bit count, 13 invalid, 16-31 distance base.
 enum : uint32_t { K_LIT = 0, K_LEN = 1, K_EOB = 2, K_BAD = 3 };
+constexpr uint32_t kBadLL = 1u | (1u << 5) | (K_BAD << 9);   // invalid litlen code: spans 1 bit
+constexpr uint32_t kBadD = 1u | (1u << 5) | (1u << 13);      // invalid distance code
 __device__ __forceinline__ uint32_t ll_entry(uint32_t sym, uint32_t len) {
-  if (sym < 256) return len | (K_LIT << 4) | (sym << 8);
-  if (sym == 256) return len | (K_EOB << 4);
+  if (sym < 256) return len | (len << 5) | (K_LIT << 9) | (sym << 16);
+  if (sym == 256) return len | (len << 5) | (K_EOB << 9);
   if (sym <= 285) {
-    const uint32_t i = sym - 257;
-    return len | (K_LEN << 4) | (uint32_t(c_len_base[i]) << 8) | (uint32_t(c_len_extra[i]) << 17);
+    const uint32_t i = sym - 257, xb = c_len_extra[i];
+    return (len + xb) | (len << 5) | (K_LEN << 9) | (xb << 11) | (uint32_t(c_len_base[i]) << 16);
   }
-  return K_BAD << 4;
+  return kBadLL;
 }
 __device__ __forceinline__ uint32_t d_entry(uint32_t sym, uint32_t len) {
-  if (sym < 30) return len | (uint32_t(c_dist_base[sym]) << 8) | (uint32_t(c_dist_extra[sym]) << 24);
-  return K_BAD << 4;
+  if (sym < 30) {
+    const uint32_t dx = c_dist_extra[sym];
+    return (len + dx) | (len << 5) | (dx << 9) | (uint32_t(c_dist_base[sym]) << 16);
+  }
+  return kBadD;
 }
 
 struct CanonTab {        // canonical code description of one table (RFC 1951 §3.2.2)
@@ -118,7 +124,7 @@ struct HuffSmem {
   uint16_t sorted_ll[288];
   uint16_t sorted_d[32];
   uint8_t lens[320];     // 286 litlen + 30 dist code lengths
-  uint32_t bad;
+  uint32_t bad, next;
   uint32_t wlits[16];
   uint64_t wbits[16];
   uint64_t carry_bits;
@@ -184,105 +190,72 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// LSB-first bit reader of one bitstream segment, written so that the lanes of a warp never diverge in it.
-// The stream is staged through the thread's own ring of NC 16-byte chunks in shared memory by cp.async
-// (LDGSTS). refill(), called once per decode iteration by every lane, issues (predicated) the next chunk while
-// it is at most NC-2 chunks ahead of the words in use, commits one group and waits until all but the newest
-// kWaitIters groups are complete: a chunk is issued ITS iterations (<= 49 bits each) before its first word is
-// read, so the global-load latency never sits on the per-symbol chain and no lane
-// waits on another lane's data. The 64-bit window is two registers (lo, hi) and a bit offset: peek() = one
-// funnel shift; consume(n <= 32) is branch-free (one shared load, selected when a word boundary is crossed).
-// Chunk addresses are clamped to the file (bytes past the stream are never used).
-template <uint32_t NC>
-struct BitRing {
-  static constexpr uint32_t WM = NC * 4 - 1;   // word mask of the ring
-  // a chunk issued at iteration i is first read >= 32*(4*(NC-2)-3) bits later, i.e. at iteration >= i+ITS
-  // (<= 49 bits per iteration), so the wait in iteration i+ITS-1 may leave the ITS-1 newest groups pending
-  static constexpr uint32_t ITS = (32 * (4 * (NC - 2) - 3) + 48) / 49;
-  static constexpr uint32_t kWaitIters = ITS - 1;
-  uint32_t ring;                               // shared-window address of this thread's ring
-  const uint8_t* gbase;                        // 16-aligned start of the block's bitstream
-  uint32_t gmax;                               // last valid 16-byte chunk offset from gbase
-  uint32_t w, lo, hi, pos, nextc;
-  __device__ __forceinline__ const uint8_t* chunk_addr(uint32_t c) const {
-    return gbase + min(c * 16u, gmax);
+// Window bit readers (LSB-first, RFC 1951 §3.1.1; reading R15). The decoders keep ONE register of reader state,
+// the absolute bit position `at` in the block's bitstream; window(at) returns the 64 stream bits starting there
+// as (r0, r1) from three 32-bit words and two funnel shifts. A symbol (<= 48 bits with its extra bits and its
+// distance) is decoded from one window, so there is no per-symbol refill or consume bookkeeping.
+//   SmemBits   the bits of the current work unit were staged in shared memory by cp.async before decoding
+//   GlobalBits fallback for a unit larger than the stage: the words come straight from the file (L1/L2)
+__device__ __forceinline__ uint32_t ldsw(uint32_t a) {     // shared load without a memory clobber
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+struct SmemBits {
+  uint32_t base;   // shared-window address holding stream bit `org` at bit 0
+  uint32_t org;    // 128-aligned absolute bit position of the stage start
+  __device__ __forceinline__ void window(uint32_t at, uint32_t& r0, uint32_t& r1) const {
+    const uint32_t rel = at - org;
+    const uint32_t p = base + ((rel >> 5) << 2);
+    const uint32_t w0 = ldsw(p), w1 = ldsw(p + 4), w2 = ldsw(p + 8);
+    r0 = __funnelshift_r(w0, w1, rel);
+    r1 = __funnelshift_r(w1, w2, rel);
   }
-  __device__ __forceinline__ void init(uint32_t r, const uint8_t* gb, uint64_t gm, uint32_t start) {
-    ring = r;
-    gbase = gb;
-    gmax = uint32_t(gm < 0xfffffff0ull ? gm : 0xfffffff0ull);
-    w = start >> 5;
-    pos = start & 31;
-    const uint32_t c0 = w >> 2;
-#pragma unroll
-    for (uint32_t k = 0; k + 1 < NC; ++k) cp_async16(ring + ((c0 + k) % NC) * 16u, chunk_addr(c0 + k));
-    cp_commit();
-    cp_wait_n<0>();
-    nextc = c0 + NC - 1;
-    lo = lds32(ring + ((w & WM) << 2));
-    hi = lds32(ring + (((w + 1) & WM) << 2));
+};
+struct GlobalBits {
+  const uint32_t* g;   // 16-byte aligned start of the block's bitstream; >= 16 readable bytes follow its end
+  __device__ __forceinline__ void window(uint32_t at, uint32_t& r0, uint32_t& r1) const {
+    const uint32_t* p = g + (at >> 5);
+    const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
+    r0 = __funnelshift_r(w0, w1, at);
+    r1 = __funnelshift_r(w1, w2, at);
   }
-  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_r(lo, hi, pos); }
-  __device__ __forceinline__ void consume(uint32_t n) {
-    pos += n;
-    const bool c = pos >= 32;
-    pos -= c ? 32u : 0u;
-    w += c ? 1u : 0u;
-    const uint32_t nh = lds32(ring + (((w + 1) & WM) << 2));
-    lo = c ? hi : lo;
-    hi = c ? nh : hi;
-  }
-  __device__ __forceinline__ void refill() {
-    const uint32_t p = nextc <= ((w + 1) >> 2) + NC - 2 ? 1u : 0u;
-    const uint32_t sa = ring + (nextc % NC) * 16u;
-    const uint8_t* ga = chunk_addr(nextc);
-    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q cp.async.cg.shared.global [%0], [%1], 16;\n}\n"
-                 ::"r"(sa), "l"(ga), "r"(p) : "memory");
-    nextc += p;
-    cp_commit();
-    cp_wait_n<kWaitIters>();
-  }
-  __device__ __forceinline__ uint32_t at() const { return w * 32 + pos; }  // absolute bit position
-  __device__ __forceinline__ void drain() const { cp_wait_n<0>(); }
 };
 
-// One decode iteration (one table lookup per symbol): a litlen symbol and, for a length code, its
-// extra bits, the distance symbol and its extra bits. kind: K_LIT / K_LEN / K_EOB / K_BAD.
-struct Step {
-  uint32_t kind, L, dist, byte, bad;
+struct Luts {
+  uint32_t ll, d, mask;   // shared-window addresses of the two tables, index mask
+  const HuffSmem* sm;     // canonical description (codes longer than the table index)
 };
-template <bool LONG, class BR>
-__device__ __forceinline__ Step decode_step(BR& in, uint32_t lut_ll_s, uint32_t lut_d_s, uint32_t lmask,
-                                            const HuffSmem& sm) {
-  Step st;
-  in.refill();
-  const uint32_t pk = in.peek();
-  uint32_t ent = lds32(lut_ll_s + ((pk & lmask) << 2));
-  uint32_t len = ent & 15u;
-  if (LONG && len == 0) {                                      // code longer than the table index
-    const int sl = canon_slow(pk, sm.tab[0], sm.sorted_ll);
-    ent = sl < 0 ? (K_BAD << 4) | 1u : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-    len = ent & 15u;
+
+// One symbol (one table lookup per symbol) from the window at `at`: the litlen entry E, its extra
+// bits, and for a length code the distance entry D and its extra bits. Returns the bits it spans (>= 1; a
+// K_BAD entry spans 1 bit so that speculative lanes always progress). r0/d32 are kept for value extraction.
+template <bool LONG, class RD>
+__device__ __forceinline__ uint32_t sym_decode(const RD& rd, uint32_t at, const Luts& t, uint32_t& E, uint32_t& D,
+                                               uint32_t& r0, uint32_t& d32) {
+  uint32_t r1;
+  rd.window(at, r0, r1);
+  E = ldsw(t.ll + ((r0 & t.mask) << 2));
+  if (LONG && (E & 31u) == 0) {                                  // code longer than the table index
+    const int sl = canon_slow(r0, t.sm->tab[0], t.sm->sorted_ll);
+    E = sl < 0 ? kBadLL : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
   }
-  st.kind = (ent >> 4) & 3u;
-  const bool isl = st.kind == K_LEN;
-  const uint32_t xb = isl ? (ent >> 17) & 7u : 0u;
-  st.L = ((ent >> 8) & 511u) + ((pk >> len) & ((1u << xb) - 1u));
-  st.byte = (ent >> 8) & 255u;
-  in.consume(len + xb);
-  const uint32_t pd = in.peek();
-  uint32_t de = lds32(lut_d_s + ((pd & lmask) << 2));
-  uint32_t dl = de & 15u;
-  if (LONG && isl && dl == 0) {
-    const int sl = canon_slow(pd, sm.tab[1], sm.sorted_d);
-    de = sl < 0 ? (K_BAD << 4) | 1u : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-    dl = de & 15u;
+  const uint32_t t1 = E & 31u;
+  d32 = __funnelshift_r(r0, r1, t1);
+  D = ldsw(t.d + ((d32 & t.mask) << 2));
+  const bool isl = ((E >> 9) & 3u) == K_LEN;
+  if (LONG && isl && (D & 31u) == 0) {
+    const int sl = canon_slow(d32, t.sm->tab[1], t.sm->sorted_d);
+    D = sl < 0 ? kBadD : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
   }
-  const uint32_t dx = (de >> 24) & 15u;
-  st.dist = ((de >> 8) & 0xffffu) + ((pd >> dl) & ((1u << dx) - 1u));
-  in.consume(isl ? dl + dx : 0u);
-  st.bad = isl && ((de >> 4) & 3u) == K_BAD;
-  return st;
+  return t1 + (isl ? (D & 31u) : 0u);
+}
+__device__ __forceinline__ uint32_t sym_kind(uint32_t E) { return (E >> 9) & 3u; }
+__device__ __forceinline__ uint32_t sym_len(uint32_t E, uint32_t r0) {      // match length (K_LEN)
+  return (E >> 16) + ((r0 >> ((E >> 5) & 15u)) & ((1u << ((E >> 11) & 7u)) - 1u));
+}
+__device__ __forceinline__ uint32_t sym_dist(uint32_t D, uint32_t d32) {
+  return (D >> 16) + ((d32 >> ((D >> 5) & 15u)) & ((1u << ((D >> 9) & 15u)) - 1u));
 }
 
 // a1 + a3 for one data block, whole CTA: unpack the nibble code lengths, canonical tables (warp 0; counts,
@@ -291,7 +264,7 @@ __device__ __forceinline__ Step decode_step(BR& in, uint32_t lut_ll_s, uint32_t 
 template <bool LONG>
 __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, const uint8_t* pl, const Args& a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lut_n = 1u << a.lut_bits;
-  if (tid == 0) { sm.bad = 0; sm.carry_bits = 0; sm.carry_lits = 0; }
+  if (tid == 0) { sm.bad = 0; sm.next = 0; sm.carry_bits = 0; sm.carry_lits = 0; }
   if (tid < 16) {
     sm.tab[0].count[tid] = 0; sm.tab[0].running[tid] = 0;
     sm.tab[1].count[tid] = 0; sm.tab[1].running[tid] = 0;
@@ -353,7 +326,7 @@ __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, co
     const uint32_t idx = i - (t ? lut_n : 0u);
     const uint32_t v = __brev(idx) >> (32 - LB);      // code bits, first stream bit most significant
     const CanonTab& T = sm.tab[t];
-    uint32_t ent = LONG ? 0u : ((K_BAD << 4) | 1u);    // unresolved: long code (LONG) or invalid
+    uint32_t ent = LONG ? 0u : (t ? kBadD : kBadLL);  // unresolved: long code (LONG) or invalid
     for (uint32_t l = 1; l <= LB; ++l) {
       const uint32_t code = v >> (LB - l);
       if (code - T.first[l] < T.count[l]) {
@@ -371,51 +344,74 @@ __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, co
 __device__ __forceinline__ bool huff_block_ok(const Args& a, const BlockEntry& e, uint32_t ulen) {
   return payload_ok(a, e) && e.payload_len >= kTreeBytes && e.S >= 1 && e.n_sub == (e.n_seq + e.S - 1) / e.S &&
          uint64_t(e.sub_first) + e.n_sub <= a.n_sub_total && 4ull * e.n_seq + e.n_lit <= a.max_tok &&
-         e.n_lit <= ulen && e.n_seq <= ulen;
+         e.n_lit <= ulen && e.n_seq <= ulen && uint64_t(e.payload_len) * 8 < (1ull << 31);
 }
 
-// Serial decode of one whole sub-block by one thread (the paper's thread-per-sub-block scheme):
-// records at rec[0..nseq), literals at lit[0..nl). Returns 0 or a CorruptStream detail code.
-template <bool LONG, class BR>
-__device__ uint32_t decode_sub_serial(BR& in, uint32_t lut_ll_s, uint32_t lut_d_s, uint32_t lmask, const HuffSmem& sm,
-                                      const Args& a, uint32_t* rec, uint8_t* lit, uint32_t nseq, uint32_t nl,
-                                      bool last, uint32_t bsz) {
-  const uint32_t mm1 = a.min_match - 1, b0 = in.at();
+// Record of a closed sequence (FORMAT.md §2): lit_len | mcode << 10 | (dist - 1) << 16.
+__device__ __forceinline__ uint32_t seq_record(uint32_t run, uint32_t L, uint32_t dist, uint32_t mm1) {
+  return run | ((L - mm1) << 10) | ((dist - 1) << 16);
+}
+
+// Serial decode of one whole sub-block from bit `at` by one thread (the paper's thread-per-sub-block scheme,
+// P:70-72): records at rec[0..nseq), literals at lit[0..nl). Returns 0 or a CorruptStream detail code.
+template <bool LONG, class RD>
+__device__ uint32_t decode_sub_serial(const RD& rd, const Luts& t, const Args& a, uint32_t at, uint32_t* rec,
+                                      uint8_t* lit, uint32_t nseq, uint32_t nl, bool last, uint32_t bsz) {
+  const uint32_t mm1 = a.min_match - 1, b0 = at;
   uint32_t si = 0, lw = 0, run = 0, bad = 0, kind = K_LIT;
   for (;;) {
     if (!last && si >= nseq) break;
-    const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-    kind = st.kind;
+    uint32_t E, D, r0, d32;
+    at += sym_decode<LONG>(rd, at, t, E, D, r0, d32);
+    kind = sym_kind(E);
     const bool isl = kind == K_LEN, islit = kind == K_LIT;
-    if (islit && lw < nl) lit[lw] = uint8_t(st.byte);
+    if (islit && lw < nl) lit[lw] = uint8_t(E >> 16);
     lw += islit ? 1u : 0u;
     run += islit ? 1u : 0u;
     // R10/R16: a sequence closes at a length code, at 1023 literals, or at EOB with pending literals
     const bool close = isl || (islit && run == kMaxLitRun) || (kind == K_EOB && run != 0);
-    if (close && si < nseq) rec[si] = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
+    const uint32_t L = sym_len(E, r0);
+    if (close && si < nseq) rec[si] = isl ? seq_record(run, L, sym_dist(D, d32), mm1) : run;
     si += close ? 1u : 0u;
     run = close ? 0u : run;
-    bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match));
-    if (kind >= K_EOB || lw > nl || si > nseq || in.at() - b0 > bsz) break;
+    bad |= isl && ((D >> 13) & 1u || L < a.min_match || L > a.max_match);
+    if (kind >= K_EOB || lw > nl || si > nseq || at - b0 > bsz) break;
   }
   if (bad) return 6;
   if (kind == K_BAD) return 2;
   if (kind == K_EOB && !last) return 7;
-  if (si != nseq || run != 0 || lw != nl || in.at() - b0 != bsz) return 9;
+  if (si != nseq || run != 0 || lw != nl || at - b0 != bsz) return 9;
   return 0;
 }
 
+// The unit of bits a CTA stages: [gs, ge) of the block's bitstream, as 16-byte chunks c0.. plus one chunk of
+// look-ahead for the 64-bit window. All threads issue cp.async (coalesced 16-byte LDGSTS), then wait; the
+// caller's __syncthreads publishes the stage. Returns false (uniformly) when it does not fit `cap` bytes.
+__device__ __forceinline__ bool stage_bits(uint32_t stage_s, uint32_t cap, const uint8_t* gbits, uint64_t gmax,
+                                           uint64_t gs, uint64_t ge, SmemBits& rd) {
+  const uint64_t c0 = gs >> 7, nch = ((ge + 127) >> 7) - c0 + 1;
+  if (nch * 16 > cap) return false;
+  for (uint32_t i = threadIdx.x; i < nch; i += blockDim.x)
+    cp_async16(stage_s + i * 16u, gbits + (c0 + i < (gmax >> 4) ? (c0 + i) * 16ull : gmax));
+  cp_commit();
+  cp_wait_n<0>();
+  rd.base = stage_s;
+  rd.org = uint32_t(c0 * 128);
+  return true;
+}
+
 // ------------------------------------------------------------------ K1a: thread-per-sub-block decode (Bit)
-// One CTA per data block; thread k decodes sub-blocks k, k+blockDim, ... (used when sub-blocks are small,
-// e.g. the paper's 16-sequence sub-blocks, where there are thousands per block).
+// One CTA per data block; in round r thread t decodes sub-block r*T + t (used when sub-blocks are small, e.g.
+// the paper's 16-sequence sub-blocks, where there are thousands per block). The T sub-blocks of a
+// round are contiguous in the bitstream, so the round stages their bits in shared memory first.
 template <bool LONG>
-__global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
+__global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t stage_cap) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
   const uint32_t lut_n = 1u << a.lut_bits;
   uint32_t* lut_d = lut_ll + lut_n;
-  const uint32_t rings_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n));   // 128 B per thread
+  const uint32_t stage_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n));
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
@@ -428,14 +424,16 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
     if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
     return;
   }
-  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
+  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
+  const Luts t{lut_ll_s, lut_ll_s + lut_n * 4, lut_n - 1, &sm};
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint8_t* subt = a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total;
   uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
   uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
   uint8_t* lit_base = tok + 4ull * e.n_seq;
+  const uint8_t* gbits = pl + kTreeBytes;
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
-  // a2: CTA-wide exclusive scans of the sub-block bit sizes and literal counts, chunk by chunk
+  // a2: CTA-wide exclusive scans of the sub-block bit sizes and literal counts, round by round
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
     uint32_t bsz = 0, nl = 0;
@@ -451,9 +449,12 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
     uint64_t pre_b = sm.carry_bits;
     uint32_t pre_l = sm.carry_lits;
     for (uint32_t w = 0; w < warp; ++w) { pre_b += sm.wbits[w]; pre_l += sm.wlits[w]; }
+    const uint64_t gs = sm.carry_bits;
     uint64_t tot_b = sm.carry_bits;
     uint32_t tot_l = sm.carry_lits;
     for (uint32_t w = 0; w < nwarps; ++w) { tot_b += sm.wbits[w]; tot_l += sm.wlits[w]; }
+    SmemBits srd;
+    const bool staged = tot_b <= bit_limit && stage_bits(stage_s, stage_cap, gbits, gmax, gs, tot_b, srd);
     __syncthreads();
     if (tid == 0) { sm.carry_bits = tot_b; sm.carry_lits = tot_l; }
     const uint64_t start = pre_b + ib - bsz;
@@ -464,16 +465,16 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
       const uint32_t seq0 = k * e.S;
       const uint32_t nseq = (k + 1 == e.n_sub) ? e.n_seq - seq0 : e.S;
       if (!err) {
-        BitRing<8> in;
-        in.init(rings_s + tid * 128, pl + kTreeBytes, gmax, uint32_t(start));
-        err = decode_sub_serial<LONG>(in, lut_ll_s, lut_d_s, lut_n - 1, sm, a, rec_base + seq0, lit_base + lstart,
-                                      nseq, nl, k + 1 == e.n_sub, bsz);
-        in.drain();
+        err = staged ? decode_sub_serial<LONG>(srd, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq,
+                                               nl, k + 1 == e.n_sub, bsz)
+                     : decode_sub_serial<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a,
+                                               uint32_t(start), rec_base + seq0, lit_base + lstart, nseq, nl,
+                                               k + 1 == e.n_sub, bsz);
       }
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
+    __syncthreads();
   }
-  __syncthreads();
   if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
 }
 
@@ -483,28 +484,207 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a) {
 // sub-block (c = ceil(bits/32)), i.e. usually inside a codeword, and decodes speculatively to the first symbol
 // boundary at or after its chunk end, recording its first kRec iteration boundaries. Canonical prefix codes
 // self-synchronise: lane p's path joins the true path when the true exit position of lane p-1 is one of its
-// recorded boundaries; otherwise that lane re-decodes from the true position (a rare serial fix-up). Then warp
-// scans give every lane its record and literal offsets and pass 2 decodes again from the true starts, writing
-// records and literals. Sequences close only at length codes here (a literal run reaching 1023 bytes, R10,
-// makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
-constexpr uint32_t kRec = 32;            // recorded iteration boundaries per lane (self-sync window)
-constexpr uint32_t kSpecRing = 4;        // 16-byte chunks per lane bit ring
+// recorded boundaries; otherwise lane p-1 keeps decoding into lane p+1's chunk, and so on (hand-over chain).
+// Then warp scans give every lane its record and literal offsets and pass 2 decodes again from the true starts,
+// writing records and literals. Sequences close only at length codes here (a literal run reaching 1023 bytes,
+// R10, makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
+// recorded iterations per lane (self-sync window). On text a lane started at a random bit needs p50 5, p99 ~37
+// symbols to join the true path; a lane that has not joined within its window costs its left neighbour a whole
+// extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
+constexpr uint32_t kRec = 64;
 constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this use one lane (serial)
+constexpr uint32_t kRecBytes = 32 * kRec;   // one u8 (bits of the iteration) per iteration per lane
+constexpr uint32_t kHuffWarps = 4;          // warps per CTA (one data block; they share its sub-blocks)
+constexpr uint32_t kStageMax = 48 * 1024;   // largest per-warp bit stage (bytes; 4 slots + tables < 227 KB)
 
-__host__ __device__ constexpr uint32_t spec_warp_bytes() { return 32 * (kSpecRing * 16 + kRec * 4); }
 
+
+// One warp decodes sub-block k (bits [S0, S0+bsz) of the block's stream) into rec[0..nseq), lit[0..nl).
+// Pass 1 keeps per lane: iterations decoded, literals, current literal run, and for its first kRec iterations
+// the bits of each (shared memory, u8) and whether it was a literal (a 64-bit register mask).
+// Anything inconsistent (counts, tail, a literal run reaching 1023 = R10) sends the sub-block to the serial
+// decoder, which is exact and reports corrupt streams.
+template <bool LONG, class RD>
+__device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args& a, uint32_t lane, uint32_t b,
+                                         uint32_t k, uint32_t recs_s, uint32_t S0, uint32_t bsz, uint32_t* rec,
+                                         uint8_t* lit, uint32_t nseq, uint32_t nl, bool last) {
+  const uint32_t mm1 = a.min_match - 1, lrange = a.max_match - a.min_match;
+  bool serial = bsz < kSpecMinBits;
+  if (!serial) {
+    // ---------------- pass 1: speculative scan of this lane's chunk
+    const uint32_t c = (bsz + 31) / 32;
+    const uint32_t sp = S0 + lane * c;
+    const uint32_t lim = S0 + min((lane + 1) * c, bsz);
+    const uint32_t endb = S0 + bsz;
+    uint32_t at = sp, cnt = 0, lits = 0, run = 0, lm0 = 0, lm1 = 0;   // lm: literal iterations of 1a (bit it)
+    auto step1 = [&](uint32_t& islit) {
+      uint32_t E, D, r0, d32;
+      const uint32_t n = sym_decode<LONG>(rd, at, t, E, D, r0, d32);
+      const uint32_t kind = sym_kind(E);
+      islit = kind == K_LIT ? 1u : 0u;
+      cnt += 1;
+      lits += islit;
+      run = kind == K_LEN ? 0u : run + islit;
+      return n;
+    };
+    // 1a: the first kRec iterations, recording the bits of each (boundary it+1 = boundary it + that)
+#pragma unroll 4
+    for (uint32_t it = 0; it < 32; ++it) {
+      uint32_t n = 0, islit = 0;
+      if (at < endb) n = step1(islit);         // never decode past the end of the sub-block
+      sts8(recs_s + it * 32 + lane, n);
+      at += n;
+      lm0 |= islit << it;
+    }
+#pragma unroll 4
+    for (uint32_t it = 32; it < kRec; ++it) {
+      uint32_t n = 0, islit = 0;
+      if (at < endb) n = step1(islit);
+      sts8(recs_s + it * 32 + lane, n);
+      at += n;
+      lm1 |= islit << (it - 32);
+    }
+    __syncwarp();
+    // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there
+    // on both paths are the same (prefix codes: same position, same state => same decode)
+    uint32_t q = lane + 1, ptr = 0, bq = (lane + 1) * c, exit_lane = 32, exit_idx = 0;  // bq: boundary ptr of q
+    for (;;) {
+      if (at >= endb) break;
+      if (at >= lim && q < 32) {
+        const uint32_t rel = at - S0;
+        while (bq < rel) {
+          if (ptr == kRec) {
+            if (++q == 32) break;
+            ptr = 0;
+            bq = q * c;
+          } else {
+            bq += lds8(recs_s + ptr * 32 + q);
+            ++ptr;
+          }
+        }
+        if (q < 32 && bq == rel) { exit_lane = q; exit_idx = ptr; break; }
+      }
+      uint32_t islit;
+      at += step1(islit);
+    }
+    // ---------------- the true path: lane 0 starts at the sub-block start (its boundary 0) and hands over to
+    // the lane it exited into, at that lane's recorded boundary; lanes it jumped over own nothing
+    uint32_t merged = 0xffffffffu, mpos = 0;   // boundary index / position where this lane's true segment starts
+    {
+      const uint32_t e_rel = at - S0;
+      uint32_t cur = 0, idx = 0, pos = 0;
+      for (uint32_t hop = 0; hop < 32 && cur < 32; ++hop) {
+        if (lane == cur) { merged = idx; mpos = pos; }
+        const uint32_t nl2 = __shfl_sync(FULL, exit_lane, cur), ni = __shfl_sync(FULL, exit_idx, cur);
+        pos = __shfl_sync(FULL, e_rel, cur);
+        cur = nl2;
+        idx = ni;
+      }
+    }
+    const bool on = merged != 0xffffffffu;
+    const bool is_tail = on && exit_lane == 32;
+    uint32_t t_start = 0, e_pos = 0, lits_t = 0, nlen_t = 0, trail_t = 0;
+    bool has_t = false;
+    if (on) {
+      // statistics of the true segment = totals at the exit minus the counts before the merge boundary (all
+      // `merged` iterations before it were decoded: the boundary lies before the sub-block end)
+      const uint32_t m0 = min(merged, 32u), m1 = merged - m0;
+      const uint32_t lits0 = __popc(lm0 & (m0 == 32 ? FULL : (1u << m0) - 1u)) +
+                             __popc(lm1 & (m1 == 32 ? FULL : (1u << m1) - 1u));
+      const uint32_t nonlit0 = merged - lits0;
+      t_start = mpos;
+      e_pos = at - S0;
+      lits_t = lits - lits0;
+      // non-literal symbols of the segment = length codes (+ the block's EOB at the very end of the tail lane)
+      nlen_t = (cnt - lits) - nonlit0 - ((last && is_tail) ? 1u : 0u);
+      has_t = nlen_t != 0;
+      trail_t = has_t ? run : lits_t;
+    }
+    // literal run entering this lane = carried across lanes without length codes:
+    // inclusive scan of (has, val) with (h2,v2)∘(h1,v1) = h2 ? (1,v2) : (h1, v1 + v2)
+    uint32_t runin;
+    {
+      uint32_t hv = has_t ? 1u : 0u, val = has_t ? trail_t : lits_t;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t h1 = __shfl_up_sync(FULL, hv, d), v1 = __shfl_up_sync(FULL, val, d);
+        if (lane >= uint32_t(d) && !hv) { hv = h1; val = v1 + val; }
+      }
+      const uint32_t vprev = __shfl_up_sync(FULL, val, 1);
+      runin = lane == 0 ? 0u : vprev;
+    }
+    // ---------------- offsets: exclusive scans of sequences (closed by length codes) and literals
+    uint32_t seqs = nlen_t;   // + the EOB-closed final literal-only sequence of the block
+    if (last && is_tail && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
+    const uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
+    const uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
+    const bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
+    serial = seq_tot != nseq || lit_tot != nl || !tail_ok;
+    if (!serial) {
+      // ---------------- pass 2: decode from the true start, write records and literals
+      uint32_t ri = seq_inc - seqs, li = lit_inc - lits_t, run2 = runin, bad = 0, maxr = 0;
+      bool saw_eob = false;
+      uint32_t at2 = S0 + t_start;
+      const uint32_t stop = S0 + e_pos;
+      while (at2 < stop) {
+        uint32_t E, D, r0, d32;
+        const uint32_t n = sym_decode<LONG>(rd, at2, t, E, D, r0, d32);
+        at2 += n;
+        const uint32_t kind = sym_kind(E);
+        if (kind == K_LIT) {
+          lit[li++] = uint8_t(E >> 16);
+          ++run2;
+        } else if (kind == K_LEN) {
+          const uint32_t L = sym_len(E, r0);
+          rec[ri++] = seq_record(run2, L, sym_dist(D, d32), mm1);
+          bad |= ((D >> 13) & 1u) | (L - a.min_match > lrange ? 1u : 0u);
+          maxr = max(maxr, run2);
+          run2 = 0;
+        } else {
+          if (kind == K_EOB) {
+            saw_eob = true;
+            if (run2 != 0 && ri < nseq) rec[ri++] = run2;
+          } else {
+            bad = 1;
+          }
+          break;
+        }
+      }
+      maxr = max(maxr, run2);
+      // R10: a literal run reaching 1023 closes a sequence, which the offsets above did not count
+      serial = __any_sync(FULL, maxr >= kMaxLitRun);
+      if (!serial) {
+        // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
+        if (bad || at2 != stop || saw_eob != (last && is_tail))
+          report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
+        return;
+      }
+      __syncwarp();
+    }
+  }
+  // ---------------- serial fallback (small sub-blocks, literal runs >= 1023, anything inconsistent): lane 0
+  // decodes all of it and validates it against the table
+  if (lane == 0) {
+    const uint32_t err = decode_sub_serial<LONG>(rd, t, a, S0, rec, lit, nseq, nl, last, bsz);
+    if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
+  }
+  __syncwarp();
+}
+
+// One CTA of kHuffWarps warps per data block: after the CTA builds the tables, each warp takes the next
+// sub-block of the block from a shared counter, stages its bits in the warp's shared-memory slot (cp.async;
+// a sub-block larger than the slot reads its bits from global memory instead) and decodes it with warp_sub.
+// No CTA barrier after the table build, so a warp never waits for another warp's sub-block.
 template <bool LONG>
-__global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
+__global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a, uint32_t stage_cap) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
   const uint32_t lut_n = 1u << a.lut_bits;
   uint32_t* lut_d = lut_ll + lut_n;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const uint32_t wbase_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + warp * spec_warp_bytes();
-  const uint32_t ring_s = wbase_s + lane * (kSpecRing * 16);           // this lane's bit ring
-  // [kRec][32] recorded boundaries: (position - lane start) | literals before it << 16 | length codes << 24
-  const uint32_t recs_s = wbase_s + 32 * kSpecRing * 16;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + warp * (kRecBytes + stage_cap);
+  const uint32_t recs_s = slot_s, stage_s = slot_s + kRecBytes;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
   if (!huff_block_ok(a, e, block_ulen(a, b))) {
@@ -516,8 +696,8 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
     if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
     return;
   }
-  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll)), lut_d_s = lut_ll_s + lut_n * 4;
-  const uint32_t lmask = lut_n - 1, mm1 = a.min_match - 1;
+  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
+  const Luts t{lut_ll_s, lut_ll_s + lut_n * 4, lut_n - 1, &sm};
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint32_t* subt = reinterpret_cast<const uint32_t*>(a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total) +
                          2ull * e.sub_first;
@@ -526,187 +706,43 @@ __global__ void __launch_bounds__(512) huff_warp_kernel(const Args a) {
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
   const uint8_t* gbits = pl + kTreeBytes;
-  const uint32_t le = (2u << lane) - 1u, lt = (1u << lane) - 1u;
-
-  for (uint32_t k = warp; k < e.n_sub; k += nwarps) {
+  for (;;) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(&sm.next, 1u);
+    k = __shfl_sync(FULL, k, 0);
+    if (k >= e.n_sub) break;
     // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
     uint64_t sb = 0;
     uint32_t sl = 0;
-    for (uint32_t j = lane; j < k; j += 32) { sb += __ldg(subt + 2 * j); sl += __ldg(subt + 2 * j + 1); }
+    for (uint32_t i = lane; i < k; i += 32) { sb += __ldg(subt + 2 * i); sl += __ldg(subt + 2 * i + 1); }
 #pragma unroll
     for (int d = 16; d; d >>= 1) { sb += __shfl_xor_sync(FULL, sb, d); sl += __shfl_xor_sync(FULL, sl, d); }
     const uint32_t bsz = __ldg(subt + 2 * k), nl = __ldg(subt + 2 * k + 1);
     const uint32_t seq0 = k * e.S;
     const bool last = k + 1 == e.n_sub;
     const uint32_t nseq = last ? e.n_seq - seq0 : e.S;
-    uint32_t* rec = rec_base + seq0;
-    uint8_t* lit = lit_base + sl;
     if (sb + bsz > bit_limit || uint64_t(sl) + nl > e.n_lit) {
       if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 1u);
       continue;
     }
-    const uint32_t S0 = uint32_t(sb);        // absolute start bit of the sub-block in the block's bitstream
-    bool serial = bsz < kSpecMinBits;
-    uint32_t t_start = 0, e_pos = 0, lits_t = 0, nlen_t = 0, lead_t = 0, trail_t = 0, maxrun = 0;
-    bool has_t = false, is_tail = false;
-    if (!serial) {
-      // ---------------- pass 1: speculative scan of this lane's chunk
-      const uint32_t c = (bsz + 31) / 32;
-      const uint32_t sp = S0 + lane * c;
-      const uint32_t lim = S0 + min((lane + 1) * c, bsz);
-      const uint32_t endb = S0 + bsz;
-      uint32_t lits = 0, nlen = 0, lead = 0, run = 0, first_len_seen = 0;
-      uint32_t lead_after_rec = 0xffffffffu;   // literals before the first length code at iteration >= kRec-1
-      BitRing<kSpecRing> in;
-      in.init(ring_s, gbits, gmax, sp);
-      auto account = [&](const Step& st, uint32_t it) {
-        in.consume(st.kind == K_BAD ? 1u : 0u);   // garbage before self-synchronisation (validated in pass 2)
-        const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
-        lits += islit ? 1u : 0u;
-        run += islit ? 1u : 0u;
-        lead = (isl && !first_len_seen) ? lits : lead;
-        lead_after_rec = (isl && it + 1 >= kRec && lead_after_rec == 0xffffffffu) ? lits : lead_after_rec;
-        first_len_seen |= isl ? 1u : 0u;
-        nlen += isl ? 1u : 0u;
-        maxrun = isl ? max(maxrun, run) : maxrun;
-        run = isl ? 0u : run;
-      };
-      // 1a: the first kRec iterations, recording each boundary (position, literals and length codes before it)
-      for (uint32_t it = 0; it < kRec; ++it) {
-        sts32(recs_s + (it * 32 + lane) * 4, (in.at() - sp) | (lits << 16) | (nlen << 24));
-        if (in.at() < endb) {                    // never decode past the end of the sub-block
-          const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-          account(st, it);
-        }
-      }
+    // stage [sb, sb + bsz) as 16-byte chunks (+1 chunk of window look-ahead) into this warp's slot
+    const uint64_t c0 = sb >> 7, nch = ((sb + bsz + 127) >> 7) - c0 + 1;
+    __syncwarp();   // the previous sub-block's readers of the slot are done
+    if (nch * 16 <= stage_cap) {
+      for (uint32_t i = lane; i < nch; i += 32)
+        cp_async16(stage_s + i * 16u, gbits + (c0 + i < (gmax >> 4) ? (c0 + i) * 16ull : gmax));
+      cp_commit();
+      cp_wait_n<0>();
       __syncwarp();
-      // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there
-      // on both paths are the same (prefix codes: same position, same state => same decode)
-      uint32_t q = lane + 1, ptr = 0, exit_lane = 32, exit_idx = 0;
-      for (uint32_t it = kRec;; ++it) {
-        const uint32_t pos = in.at();
-        if (pos >= endb) break;
-        if (pos >= lim && q < 32) {
-          const uint32_t rel = pos - S0;
-          uint32_t bq = q * c + (lds32(recs_s + (ptr * 32 + q) * 4) & 0xffffu);
-          while (bq < rel) {
-            if (++ptr == kRec) { ptr = 0; if (++q == 32) break; }
-            bq = q * c + (lds32(recs_s + (ptr * 32 + q) * 4) & 0xffffu);
-          }
-          if (q < 32 && bq == rel) { exit_lane = q; exit_idx = ptr; break; }
-        }
-        const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-        account(st, it);
-      }
-      const uint32_t trail = run;
-      if (!first_len_seen) lead = lits;
-      e_pos = in.at() - S0;
-      in.drain();
-      // ---------------- the true path: lane 0 starts at the sub-block start (its boundary 0) and hands over to
-      // the lane it exited into, at that lane's recorded boundary; lanes it jumped over own nothing
-      uint32_t merged = 0xffffffffu;   // recorded index where this lane's segment of the true path starts
-      {
-        uint32_t cur = 0, idx = 0;
-        for (uint32_t hop = 0; hop < 32 && cur < 32; ++hop) {
-          if (lane == cur) merged = idx;
-          const uint32_t nl2 = __shfl_sync(FULL, exit_lane, cur), ni = __shfl_sync(FULL, exit_idx, cur);
-          cur = nl2;
-          idx = ni;
-        }
-      }
-      const bool on = merged != 0xffffffffu;
-      is_tail = on && exit_lane == 32;
-      if (on) {
-        // statistics of the true segment = totals at the exit minus the counts before the merge boundary
-        const uint32_t cum = lds32(recs_s + (merged * 32 + lane) * 4);
-        t_start = lane * c + (cum & 0xffffu);
-        const uint32_t lits0 = (cum >> 16) & 0xffu, nlen0 = cum >> 24;
-        lits_t = lits - lits0;
-        nlen_t = nlen - nlen0;
-        has_t = nlen_t > 0;
-        trail_t = has_t ? trail : lits_t;
-        lead_t = lits_t;
-        if (has_t) {
-          if (nlen0 == 0) lead_t = lead - lits0;               // first length code of the path is after it
-          else {
-            uint32_t found = 0xffffffffu;
-            for (uint32_t r = merged + 1; r < kRec; ++r) {
-              if ((lds32(recs_s + (r * 32 + lane) * 4) >> 24) > nlen0) { found = r; break; }  // iteration r-1 was one
-            }
-            if (found != 0xffffffffu) lead_t = ((lds32(recs_s + ((found - 1) * 32 + lane) * 4) >> 16) & 0xffu) - lits0;
-            else lead_t = (lead_after_rec != 0xffffffffu ? lead_after_rec : lits) - lits0;
-          }
-        }
-      } else {
-        e_pos = t_start = 0;
-      }
-      // a literal run of >= 1023 anywhere (R10 closes sequences there): serial fallback for this sub-block
-      uint32_t runin = 0;   // run length entering this lane = carried across lanes without length codes
-      {
-        uint32_t hv = has_t ? 1u : 0u, val = has_t ? trail_t : lits_t;
-        // inclusive scan of (has, val): (h2,v2)∘(h1,v1) = h2 ? (1,v2) : (h1, v1 + v2)
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t h1 = __shfl_up_sync(FULL, hv, d), v1 = __shfl_up_sync(FULL, val, d);
-          if (lane >= uint32_t(d) && !hv) { hv = h1; val = v1 + val; }
-        }
-        const uint32_t vprev = __shfl_up_sync(FULL, val, 1);
-        runin = lane == 0 ? 0u : vprev;
-      }
-      const bool longrun = maxrun >= kMaxLitRun || trail_t >= kMaxLitRun || runin + lead_t >= kMaxLitRun;
-      serial = __any_sync(FULL, longrun);
-      if (!serial) {
-        // ---------------- offsets: exclusive scans of sequences (closed by length codes) and literals
-        uint32_t seqs = nlen_t;   // + the EOB-closed final literal-only sequence of the block
-        if (last && is_tail && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
-        const uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
-        const uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
-        const bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
-        if (seq_tot != nseq || lit_tot != nl || !tail_ok) {
-          if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 9u);
-          continue;
-        }
-        // ---------------- pass 2: decode from the true start, write records and literals
-        uint32_t run = runin, bad = 0;
-        uint32_t* rp = rec + (seq_inc - seqs);
-        uint32_t* const rend = rec + nseq;
-        uint8_t* lp = lit + (lit_inc - lits_t);
-        uint8_t* const lend = lit + nl;
-        bool eob_bad = false, saw_eob = false;
-        BitRing<kSpecRing> in;
-        in.init(ring_s, gbits, gmax, S0 + t_start);
-        const uint32_t stop = S0 + e_pos;
-        while (in.at() < stop) {
-          const Step st = decode_step<LONG>(in, lut_ll_s, lut_d_s, lmask, sm);
-          const bool isl = st.kind == K_LEN, islit = st.kind == K_LIT;
-          if (islit && lp < lend) *lp = uint8_t(st.byte);
-          lp += islit ? 1 : 0;
-          run += islit ? 1u : 0u;
-          const bool close = isl || (st.kind == K_EOB && run != 0);
-          if (close && rp < rend) *rp = isl ? (run | ((st.L - mm1) << 10) | ((st.dist - 1) << 16)) : run;
-          rp += close ? 1 : 0;
-          run = close ? 0u : run;
-          bad |= st.bad | (isl && (st.L < a.min_match || st.L > a.max_match)) | (st.kind == K_BAD);
-          if (st.kind == K_EOB) { saw_eob = true; eob_bad |= !(last && is_tail); break; }
-        }
-        const bool at_end = in.at() == stop;
-        in.drain();
-        // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
-        if (bad || eob_bad || !at_end || saw_eob != (last && is_tail)) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
-        continue;
-      }
+      warp_sub<LONG>(SmemBits{stage_s, uint32_t(c0 * 128)}, t, a, lane, b, k, recs_s, uint32_t(sb), bsz,
+                     rec_base + seq0, lit_base + sl, nseq, nl, last);
+    } else {
+      warp_sub<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a, lane, b, k, recs_s, uint32_t(sb),
+                     bsz, rec_base + seq0, lit_base + sl, nseq, nl, last);
     }
-    // ---------------- serial fallback (small sub-blocks, literal runs >= 1023): lane 0 decodes all of it
-    if (lane == 0) {
-      BitRing<kSpecRing> in;
-      in.init(ring_s, gbits, gmax, S0);
-      const uint32_t err = decode_sub_serial<LONG>(in, lut_ll_s, lut_d_s, lmask, sm, a, rec, lit, nseq, nl, last, bsz);
-      in.drain();
-      if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
-    }
-    __syncwarp();
   }
 }
+
 
 // ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
 //
@@ -1331,7 +1367,8 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   int s = strategy & GOMP_STRAT_MASK;
   const bool stats = (strategy & GOMP_FLAG_STATS) != 0;
   const bool decode_only = (strategy & GOMP_FLAG_DECODE_ONLY) != 0, lz77_only = (strategy & GOMP_FLAG_LZ77_ONLY) != 0;
-  if (strategy & ~(GOMP_STRAT_MASK | GOMP_FLAG_STATS | GOMP_FLAG_DECODE_ONLY | GOMP_FLAG_LZ77_ONLY)) return GOMP_ERR_INVALID_ARG;
+  if (strategy & ~(GOMP_STRAT_MASK | GOMP_FLAG_STATS | GOMP_FLAG_DECODE_ONLY | GOMP_FLAG_LZ77_ONLY |
+                   GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP)) return GOMP_ERR_INVALID_ARG;
   if (decode_only && lz77_only) return GOMP_ERR_INVALID_ARG;
   if (s == GOMP_STRAT_AUTO) s = info->de ? GOMP_STRAT_DE : GOMP_STRAT_MRR;
   if (s != GOMP_STRAT_DE && s != GOMP_STRAT_MRR && s != GOMP_STRAT_SC) return GOMP_ERR_INVALID_ARG;
@@ -1376,30 +1413,39 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const uint64_t avg_bits = info->n_sub_total ? (info->file_len - info->payload_base) * 8 / info->n_sub_total : 0;
     const bool LONGc = info->cwl > a.lut_bits;
     const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << a.lut_bits) * sizeof(uint32_t);
-    if (avg_bits >= 4 * kSpecMinBits) {
-      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode
-      const uint32_t nw = uint32_t(std::min<uint64_t>(16, std::max<uint64_t>(1, avg_sub)));
-      const size_t smem = tabs + size_t(nw) * spec_warp_bytes();
+    const int force = strategy & (GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP);
+    const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= 4 * kSpecMinBits;
+    const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
+    if (use_warp) {
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode; per
+      // warp a bit stage of 1.3x the mean sub-block (+ slack)
+      const uint32_t nw = kHuffWarps;
+      const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * 13 / 10 + 96)));
+      const size_t smem = tabs + size_t(nw) * (kRecBytes + cap);
+      const uint32_t grid = nblk;
       if (LONGc) {
         cudaFuncSetAttribute(huff_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<true><<<nblk, 32 * nw, smem, st>>>(a);
+        huff_warp_kernel<true><<<grid, 32 * nw, smem, st>>>(a, cap);
       } else {
         cudaFuncSetAttribute(huff_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<false><<<nblk, 32 * nw, smem, st>>>(a);
+        huff_warp_kernel<false><<<grid, 32 * nw, smem, st>>>(a, cap);
       }
     } else {
-      // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block
+      // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block, rounds
+      // of nt sub-blocks staged together
       const uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
-      const size_t smem = tabs + size_t(nt) * 128;
+      const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * nt * 3 / 2 + 512)));
+      const size_t smem = tabs + cap;
       if (LONGc) {
         cudaFuncSetAttribute(huff_thread_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_thread_kernel<true><<<nblk, nt, smem, st>>>(a);
+        huff_thread_kernel<true><<<nblk, nt, smem, st>>>(a, cap);
       } else {
         cudaFuncSetAttribute(huff_thread_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_thread_kernel<false><<<nblk, nt, smem, st>>>(a);
+        huff_thread_kernel<false><<<nblk, nt, smem, st>>>(a, cap);
       }
     }
-    if (decode_only) return cudaGetLastError() == cudaSuccess ? GOMP_OK : GOMP_ERR_CUDA;
+    if (cudaGetLastError() != cudaSuccess) return GOMP_ERR_CUDA;
+    if (decode_only) return GOMP_OK;
   }
   switch (s) {
     case GOMP_STRAT_DE: {

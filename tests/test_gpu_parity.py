@@ -30,11 +30,11 @@ def _gpu(c, strategy="auto", **kw):
     return gomp.decompress(torch.as_tensor(np.asarray(c)).to(DEV), strategy=strategy, **kw)
 
 
-def _check(c, x, strategies):
+def _check(c, x, strategies, **kw):
     ref = oracle.decompress(np.asarray(c))
     assert np.array_equal(ref, x)
     for s in strategies:
-        y = _gpu(c, s).cpu().numpy()
+        y = _gpu(c, s, **kw).cpu().numpy()
         assert y.shape == ref.shape
         if not np.array_equal(y, ref):
             bad = np.flatnonzero(y != ref)
@@ -276,3 +276,15 @@ def test_warp_speculative_short_chunks(kind, bs, k):
     x = _data(kind, 2_000_003, seed=21)
     c = gomp.compress(x, mode="bit", de=True, block_size=bs, sub_block_seqs=0, sub_blocks_per_block=k)
     _check(c, x, ["auto"])
+
+
+@pytest.mark.parametrize("kind", ["wiki", "matrix", "nested8", "random", "zeros"])
+@pytest.mark.parametrize("sub", [("k", 16), ("k", 3), ("S", 16), ("S", 200)])
+@pytest.mark.parametrize("huff", ["thread", "warp"])
+def test_forced_decoder_variant(kind, sub, huff):
+    """Both Bit decoders (thread per sub-block, warp per sub-block) on every sub-block shape, whichever one the
+    launcher would pick: same output as the oracle, bit for bit."""
+    x = _data(kind, 700_001, seed=31)
+    kw = dict(sub_blocks_per_block=sub[1], sub_block_seqs=0) if sub[0] == "k" else dict(sub_block_seqs=sub[1])
+    c = gomp.compress(x, mode="bit", de=True, block_size=131072, **kw)
+    _check(c, x, ["auto"], huff=huff)
