@@ -178,6 +178,9 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
@@ -478,43 +481,64 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
   if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
 }
 
-// ------------------------------------------------------------------ K1b: warp-per-sub-block speculative decode
+// ------------------------------------------------------------------ K1b: group-per-sub-block speculative decode
 // B200 answer to "few, long sub-blocks" (BASELINE C2: 16 sub-blocks of ~6 KB per 256 KiB block gives only 16
-// serial chains per block). One warp decodes one sub-block with its 32 lanes: lane p starts at bit p*c of the
-// sub-block (c = ceil(bits/32)), i.e. usually inside a codeword, and decodes speculatively to the first symbol
-// boundary at or after its chunk end, recording its first kRec iteration boundaries. Canonical prefix codes
-// self-synchronise: lane p's path joins the true path when the true exit position of lane p-1 is one of its
-// recorded boundaries; otherwise lane p-1 keeps decoding into lane p+1's chunk, and so on (hand-over chain).
-// Then warp scans give every lane its record and literal offsets and pass 2 decodes again from the true starts,
-// writing records and literals. Sequences close only at length codes here (a literal run reaching 1023 bytes,
-// R10, makes the warp fall back to the serial decoder for that sub-block). Same output as K1a, bit for bit.
-// recorded iterations per lane (self-sync window). On text a lane started at a random bit needs p50 5, p99 ~37
+// serial chains per block). A group of G warps (V = 32G virtual lanes) decodes one sub-block whose bits are
+// staged in shared memory: lane p starts at bit p*c of the sub-block (c = ceil(bits/V)), i.e. usually inside a
+// codeword, and decodes speculatively to the first symbol boundary at or after its chunk end, recording its
+// first kRec iterations. Canonical prefix codes self-synchronise: lane p's path joins the true path when the
+// true exit position of lane p-1 is one of its recorded boundaries; otherwise lane p-1 keeps decoding into lane
+// p+1's chunk, and so on (hand-over chain). Then group scans give every lane its record and literal offsets and
+// pass 2 decodes again from the true starts, writing records and literals. Sequences close only at length codes
+// here; anything inconsistent (counts, tail, a literal run reaching 1023 = R10) sends the sub-block to the serial
+// decoder, which is exact and reports corrupt streams. Same output as K1a, bit for bit.
+//
+// Recorded iterations per lane (self-sync window): on text a lane started at a random bit needs p50 5, p99 ~37
 // symbols to join the true path; a lane that has not joined within its window costs its left neighbour a whole
 // extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
 constexpr uint32_t kRec = 64;
-constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below this use one lane (serial)
-constexpr uint32_t kRecBytes = 32 * kRec;   // one u8 (bits of the iteration) per iteration per lane
-constexpr uint32_t kHuffWarps = 4;          // warps per CTA (one data block; they share its sub-blocks)
-constexpr uint32_t kStageMax = 48 * 1024;   // largest per-warp bit stage (bytes; 4 slots + tables < 227 KB)
+constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below G*this use one lane (serial)
+constexpr uint32_t kHuffWarps = 16;         // warps per CTA (one data block; its groups share its sub-blocks)
+constexpr uint32_t kHuffG = 2;              // warps per sub-block group
+constexpr uint32_t kXsBytes = 1024;         // per-group exchange area (shared memory)
+constexpr uint32_t kStageMax = 48 * 1024;   // largest per-group bit stage (bytes)
+constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per CTA
+// exchange area layout (bytes): [0, 8V) exit records; 768 sub-block index; 784.. per-warp aggregates
+constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912;
+static_assert(8 * 32 * kHuffG <= kXsK && kHuffWarps % kHuffG == 0, "exchange area layout");
 
+__host__ __device__ constexpr uint32_t group_slot_bytes(uint32_t G, uint32_t stage_cap) {
+  return 32 * G * kRec + kXsBytes + stage_cap;
+}
 
+// group barrier (named barrier `bar`, 32G threads). __syncwarp first: the warp must arrive converged, or the
+// code after it may keep running lane by lane (measured: 3 threads per instruction in pass 2 without it).
+template <uint32_t G>
+__device__ __forceinline__ void gsync(uint32_t bar) {
+  __syncwarp();
+  if (G > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(32 * G) : "memory");
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v; asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory"); return v;
+}
 
-// One warp decodes sub-block k (bits [S0, S0+bsz) of the block's stream) into rec[0..nseq), lit[0..nl).
+// One group decodes sub-block k (bits [S0, S0+bsz) of the block's stream) into rec[0..nseq), lit[0..nl).
 // Pass 1 keeps per lane: iterations decoded, literals, current literal run, and for its first kRec iterations
 // the bits of each (shared memory, u8) and whether it was a literal (a 64-bit register mask).
-// Anything inconsistent (counts, tail, a literal run reaching 1023 = R10) sends the sub-block to the serial
-// decoder, which is exact and reports corrupt streams.
-template <bool LONG, class RD>
-__device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args& a, uint32_t lane, uint32_t b,
-                                         uint32_t k, uint32_t recs_s, uint32_t S0, uint32_t bsz, uint32_t* rec,
-                                         uint8_t* lit, uint32_t nseq, uint32_t nl, bool last) {
+template <bool LONG, uint32_t G, class RD>
+__device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Args& a, uint32_t vl, uint32_t bar,
+                                          uint32_t recs_s, uint32_t xs_s, uint32_t b, uint32_t k, uint32_t S0,
+                                          uint32_t bsz, uint32_t* rec, uint8_t* lit, uint32_t nseq, uint32_t nl,
+                                          bool last) {
+  constexpr uint32_t V = 32 * G;
+  const uint32_t lane = vl & 31, wg = vl >> 5;
   const uint32_t mm1 = a.min_match - 1, lrange = a.max_match - a.min_match;
-  bool serial = bsz < kSpecMinBits;
+  bool serial = bsz < kSpecMinBits * G;
   if (!serial) {
     // ---------------- pass 1: speculative scan of this lane's chunk
-    const uint32_t c = (bsz + 31) / 32;
-    const uint32_t sp = S0 + lane * c;
-    const uint32_t lim = S0 + min((lane + 1) * c, bsz);
+    const uint32_t c = (bsz + V - 1) / V;
+    const uint32_t sp = S0 + vl * c;
+    const uint32_t lim = S0 + min((vl + 1) * c, bsz);
     const uint32_t endb = S0 + bsz;
     uint32_t at = sp, cnt = 0, lits = 0, run = 0, lm0 = 0, lm1 = 0;   // lm: literal iterations of 1a (bit it)
     auto step1 = [&](uint32_t& islit) {
@@ -532,7 +556,7 @@ __device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args
     for (uint32_t it = 0; it < 32; ++it) {
       uint32_t n = 0, islit = 0;
       if (at < endb) n = step1(islit);         // never decode past the end of the sub-block
-      sts8(recs_s + it * 32 + lane, n);
+      sts8(recs_s + it * V + vl, n);
       at += n;
       lm0 |= islit << it;
     }
@@ -540,49 +564,60 @@ __device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args
     for (uint32_t it = 32; it < kRec; ++it) {
       uint32_t n = 0, islit = 0;
       if (at < endb) n = step1(islit);
-      sts8(recs_s + it * 32 + lane, n);
+      sts8(recs_s + it * V + vl, n);
       at += n;
       lm1 |= islit << (it - 32);
     }
-    __syncwarp();
+    gsync<G>(bar);
     // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there
     // on both paths are the same (prefix codes: same position, same state => same decode)
-    uint32_t q = lane + 1, ptr = 0, bq = (lane + 1) * c, exit_lane = 32, exit_idx = 0;  // bq: boundary ptr of q
+    uint32_t q = vl + 1, ptr = 0, bq = (vl + 1) * c, exit_vl = V, exit_idx = 0;  // bq: boundary ptr of lane q
     for (;;) {
       if (at >= endb) break;
-      if (at >= lim && q < 32) {
+      if (at >= lim && q < V) {
         const uint32_t rel = at - S0;
         while (bq < rel) {
           if (ptr == kRec) {
-            if (++q == 32) break;
+            if (++q == V) break;
             ptr = 0;
             bq = q * c;
           } else {
-            bq += lds8(recs_s + ptr * 32 + q);
+            bq += lds8(recs_s + ptr * V + q);
             ++ptr;
           }
         }
-        if (q < 32 && bq == rel) { exit_lane = q; exit_idx = ptr; break; }
+        if (q < V && bq == rel) { exit_vl = q; exit_idx = ptr; break; }
       }
       uint32_t islit;
       at += step1(islit);
     }
     // ---------------- the true path: lane 0 starts at the sub-block start (its boundary 0) and hands over to
     // the lane it exited into, at that lane's recorded boundary; lanes it jumped over own nothing
+    const uint32_t e_rel = at - S0;
     uint32_t merged = 0xffffffffu, mpos = 0;   // boundary index / position where this lane's true segment starts
-    {
-      const uint32_t e_rel = at - S0;
+    if (G == 1) {
       uint32_t cur = 0, idx = 0, pos = 0;
       for (uint32_t hop = 0; hop < 32 && cur < 32; ++hop) {
         if (lane == cur) { merged = idx; mpos = pos; }
-        const uint32_t nl2 = __shfl_sync(FULL, exit_lane, cur), ni = __shfl_sync(FULL, exit_idx, cur);
+        const uint32_t nl2 = __shfl_sync(FULL, exit_vl, cur), ni = __shfl_sync(FULL, exit_idx, cur);
         pos = __shfl_sync(FULL, e_rel, cur);
         cur = nl2;
         idx = ni;
       }
+    } else {
+      sts64(xs_s + vl * 8, exit_vl | (exit_idx << 16), e_rel);
+      gsync<G>(bar);
+      uint32_t cur = 0, idx = 0, pos = 0;
+      for (uint32_t hop = 0; hop < V && cur < V; ++hop) {
+        if (vl == cur) { merged = idx; mpos = pos; }
+        const uint2 x = lds64(xs_s + cur * 8);
+        cur = x.x & 0xffffu;
+        idx = x.x >> 16;
+        pos = x.y;
+      }
     }
     const bool on = merged != 0xffffffffu;
-    const bool is_tail = on && exit_lane == 32;
+    const bool is_tail = on && exit_vl == V;
     uint32_t t_start = 0, e_pos = 0, lits_t = 0, nlen_t = 0, trail_t = 0;
     bool has_t = false;
     if (on) {
@@ -593,7 +628,7 @@ __device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args
                              __popc(lm1 & (m1 == 32 ? FULL : (1u << m1) - 1u));
       const uint32_t nonlit0 = merged - lits0;
       t_start = mpos;
-      e_pos = at - S0;
+      e_pos = e_rel;
       lits_t = lits - lits0;
       // non-literal symbols of the segment = length codes (+ the block's EOB at the very end of the tail lane)
       nlen_t = (cnt - lits) - nonlit0 - ((last && is_tail) ? 1u : 0u);
@@ -610,16 +645,48 @@ __device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args
         const uint32_t h1 = __shfl_up_sync(FULL, hv, d), v1 = __shfl_up_sync(FULL, val, d);
         if (lane >= uint32_t(d) && !hv) { hv = h1; val = v1 + val; }
       }
+      uint32_t ph = 0, pv = 0;   // aggregate of the earlier warps of the group
+      if (G > 1) {
+        if (lane == 31) sts64(xs_s + kXsAggA + wg * 8, hv, val);
+        gsync<G>(bar);
+        for (uint32_t w = 0; w < wg; ++w) {
+          const uint2 x = lds64(xs_s + kXsAggA + w * 8);
+          if (x.x) { ph = 1; pv = x.y; } else pv += x.y;
+        }
+        if (!hv) { hv = ph; val += pv; }
+      }
       const uint32_t vprev = __shfl_up_sync(FULL, val, 1);
-      runin = lane == 0 ? 0u : vprev;
+      runin = lane == 0 ? pv : vprev;
     }
     // ---------------- offsets: exclusive scans of sequences (closed by length codes) and literals
     uint32_t seqs = nlen_t;   // + the EOB-closed final literal-only sequence of the block
     if (last && is_tail && (has_t ? trail_t : runin + lits_t) != 0) seqs += 1;
-    const uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
-    const uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
-    const bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
+    uint32_t seq_inc = warp_incl_scan_u32(seqs, lane), lit_inc = warp_incl_scan_u32(lits_t, lane);
+    uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
+    bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
+    if (G > 1) {
+      if (lane == 0) sts64(xs_s + kXsAggB + wg * 8, seq_tot | (tail_ok ? 0x80000000u : 0u), lit_tot);
+      gsync<G>(bar);
+      seq_tot = lit_tot = 0;
+      tail_ok = false;
+      for (uint32_t w = 0; w < G; ++w) {
+        const uint2 x = lds64(xs_s + kXsAggB + w * 8);
+        if (w < wg) { seq_inc += x.x & 0x7fffffffu; lit_inc += x.y; }
+        seq_tot += x.x & 0x7fffffffu;
+        lit_tot += x.y;
+        tail_ok |= (x.x >> 31) != 0;
+      }
+    }
     serial = seq_tot != nseq || lit_tot != nl || !tail_ok;
+#ifdef GOMP_DEBUG_GROUP
+    if (b == 0 && k == 0) {
+      uint32_t* dbg = reinterpret_cast<uint32_t*>(a.dst) + vl * 16;
+      dbg[0] = merged; dbg[1] = mpos; dbg[2] = e_rel; dbg[3] = exit_vl; dbg[4] = exit_idx; dbg[5] = lits_t;
+      dbg[6] = nlen_t; dbg[7] = seqs; dbg[8] = seq_inc; dbg[9] = lit_inc; dbg[10] = runin; dbg[11] = serial;
+      dbg[12] = c; dbg[13] = cnt; dbg[14] = lits; dbg[15] = bsz;
+    }
+    return;
+#endif
     if (!serial) {
       // ---------------- pass 2: decode from the true start, write records and literals
       uint32_t ri = seq_inc - seqs, li = lit_inc - lits_t, run2 = runin, bad = 0, maxr = 0;
@@ -653,38 +720,44 @@ __device__ __forceinline__ void warp_sub(const RD& rd, const Luts& t, const Args
       maxr = max(maxr, run2);
       // R10: a literal run reaching 1023 closes a sequence, which the offsets above did not count
       serial = __any_sync(FULL, maxr >= kMaxLitRun);
+      if (G > 1) {
+        if (lane == 0) sts32(xs_s + kXsAggC + wg * 4, serial ? 1u : 0u);
+        gsync<G>(bar);
+        for (uint32_t w = 0; w < G; ++w) serial |= lds32(xs_s + kXsAggC + w * 4) != 0;
+      }
       if (!serial) {
         // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
         if (bad || at2 != stop || saw_eob != (last && is_tail))
           report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 10u);
         return;
       }
-      __syncwarp();
+      gsync<G>(bar);   // pass-2 writes are done before the serial decoder rewrites the sub-block
     }
   }
   // ---------------- serial fallback (small sub-blocks, literal runs >= 1023, anything inconsistent): lane 0
   // decodes all of it and validates it against the table
-  if (lane == 0) {
+  if (vl == 0) {
     const uint32_t err = decode_sub_serial<LONG>(rd, t, a, S0, rec, lit, nseq, nl, last, bsz);
     if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
   }
-  __syncwarp();
 }
 
-// One CTA of kHuffWarps warps per data block: after the CTA builds the tables, each warp takes the next
-// sub-block of the block from a shared counter, stages its bits in the warp's shared-memory slot (cp.async;
-// a sub-block larger than the slot reads its bits from global memory instead) and decodes it with warp_sub.
-// No CTA barrier after the table build, so a warp never waits for another warp's sub-block.
-template <bool LONG>
+// One CTA of kHuffWarps warps per data block: after the CTA builds the tables, each group of G warps takes the
+// next sub-block of the block from a shared counter, stages its bits in the group's shared-memory slot
+// (cp.async; a sub-block larger than the slot reads its bits from global memory instead) and decodes it with
+// group_sub. Only group barriers after the table build: a group never waits for another group's sub-block.
+template <bool LONG, uint32_t G>
 __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a, uint32_t stage_cap) {
+  constexpr uint32_t V = 32 * G;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
   const uint32_t lut_n = 1u << a.lut_bits;
   uint32_t* lut_d = lut_ll + lut_n;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + warp * (kRecBytes + stage_cap);
-  const uint32_t recs_s = slot_s, stage_s = slot_s + kRecBytes;
+  const uint32_t grp = warp / G, vl = tid % V, bar = 1 + grp;
+  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + grp * group_slot_bytes(G, stage_cap);
+  const uint32_t recs_s = slot_s, xs_s = slot_s + V * kRec, stage_s = xs_s + kXsBytes;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
   if (!huff_block_ok(a, e, block_ulen(a, b))) {
@@ -707,9 +780,9 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
   const uint8_t* gbits = pl + kTreeBytes;
   for (;;) {
-    uint32_t k = 0;
-    if (lane == 0) k = atomicAdd(&sm.next, 1u);
-    k = __shfl_sync(FULL, k, 0);
+    if (vl == 0) sts32(xs_s + kXsK, atomicAdd(&sm.next, 1u));
+    gsync<G>(bar);
+    const uint32_t k = lds32(xs_s + kXsK);
     if (k >= e.n_sub) break;
     // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
     uint64_t sb = 0;
@@ -722,24 +795,24 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
     const bool last = k + 1 == e.n_sub;
     const uint32_t nseq = last ? e.n_seq - seq0 : e.S;
     if (sb + bsz > bit_limit || uint64_t(sl) + nl > e.n_lit) {
-      if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 1u);
-      continue;
-    }
-    // stage [sb, sb + bsz) as 16-byte chunks (+1 chunk of window look-ahead) into this warp's slot
-    const uint64_t c0 = sb >> 7, nch = ((sb + bsz + 127) >> 7) - c0 + 1;
-    __syncwarp();   // the previous sub-block's readers of the slot are done
-    if (nch * 16 <= stage_cap) {
-      for (uint32_t i = lane; i < nch; i += 32)
-        cp_async16(stage_s + i * 16u, gbits + (c0 + i < (gmax >> 4) ? (c0 + i) * 16ull : gmax));
-      cp_commit();
-      cp_wait_n<0>();
-      __syncwarp();
-      warp_sub<LONG>(SmemBits{stage_s, uint32_t(c0 * 128)}, t, a, lane, b, k, recs_s, uint32_t(sb), bsz,
-                     rec_base + seq0, lit_base + sl, nseq, nl, last);
+      if (vl == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 1u);
     } else {
-      warp_sub<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a, lane, b, k, recs_s, uint32_t(sb),
-                     bsz, rec_base + seq0, lit_base + sl, nseq, nl, last);
+      // stage [sb, sb + bsz) as 16-byte chunks (+1 chunk of window look-ahead) into the group's slot
+      const uint64_t c0 = sb >> 7, nch = ((sb + bsz + 127) >> 7) - c0 + 1;
+      if (nch * 16 <= stage_cap) {
+        for (uint32_t i = vl; i < nch; i += V)
+          cp_async16(stage_s + i * 16u, gbits + (c0 + i < (gmax >> 4) ? (c0 + i) * 16ull : gmax));
+        cp_commit();
+        cp_wait_n<0>();
+        gsync<G>(bar);
+        group_sub<LONG, G>(SmemBits{stage_s, uint32_t(c0 * 128)}, t, a, vl, bar, recs_s, xs_s, b, k, uint32_t(sb),
+                           bsz, rec_base + seq0, lit_base + sl, nseq, nl, last);
+      } else {
+        group_sub<LONG, G>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a, vl, bar, recs_s, xs_s, b, k,
+                           uint32_t(sb), bsz, rec_base + seq0, lit_base + sl, nseq, nl, last);
+      }
     }
+    gsync<G>(bar);   // the group is done with the slot (stage, records, exchange area)
   }
 }
 
@@ -1417,18 +1490,20 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= 4 * kSpecMinBits;
     const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
     if (use_warp) {
-      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): one warp per sub-block, speculative decode; per
-      // warp a bit stage of 1.3x the mean sub-block (+ slack)
-      const uint32_t nw = kHuffWarps;
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of kHuffG warps per sub-block, speculative
+      // decode; per group a bit stage of 1.3x the mean sub-block (+ slack); up to kHuffWarps/kHuffG groups per
+      // CTA, as many as the sub-blocks of a block and the shared memory allow
       const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * 13 / 10 + 96)));
-      const size_t smem = tabs + size_t(nw) * (kRecBytes + cap);
-      const uint32_t grid = nblk;
+      const size_t slot = group_slot_bytes(kHuffG, cap);
+      const uint64_t fit = (kSmemMax - tabs) / slot;
+      const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / kHuffG, fit, avg_sub})));
+      const size_t smem = tabs + ngr * slot;
       if (LONGc) {
-        cudaFuncSetAttribute(huff_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<true><<<grid, 32 * nw, smem, st>>>(a, cap);
+        cudaFuncSetAttribute(huff_warp_kernel<true, kHuffG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_warp_kernel<true, kHuffG><<<nblk, 32 * kHuffG * ngr, smem, st>>>(a, cap);
       } else {
-        cudaFuncSetAttribute(huff_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<false><<<grid, 32 * nw, smem, st>>>(a, cap);
+        cudaFuncSetAttribute(huff_warp_kernel<false, kHuffG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        huff_warp_kernel<false, kHuffG><<<nblk, 32 * kHuffG * ngr, smem, st>>>(a, cap);
       }
     } else {
       // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block, rounds
