@@ -54,6 +54,19 @@ def gen(kind, n, seed):
     return datagen.GENERATORS[kind](n, seed=seed)
 
 
+def ncu_traffic(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json, written from the capture named there), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        e = t[config][kernel]
+        return {"bytes": int(e["dram_read"] + e["dram_write"]), "source": e["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -254,21 +267,31 @@ def main():
     ms_per_step = t_total / args.steps
 
     # per-kernel times (Bit: Huffman decode and LZ77 launched separately, same stream, same events)
-    kernels = {}
+    T = gomp.token_bytes(c) if info.mode == 1 else 0   # Bit token buffer: 4 B per record + 1 B per literal
     if info.mode == 1:
-        kd = timed(lambda: gomp.decompress_into(info, d_src, out, ws, args.strategy, stream, phase="decode"), 10, 3)
-        kl = timed(lambda: gomp.decompress_into(info, d_src, out, ws, args.strategy, stream, phase="lz77"), 10, 3)
-        kernels = {"huff_decode_kernel_ms": round(statistics.mean(kd), 4), "lz77_kernel_ms": round(statistics.mean(kl), 4)}
+        kd = statistics.mean(timed(lambda: gomp.decompress_into(info, d_src, out, ws, args.strategy, stream,
+                                                                phase="decode"), 10, 3))
+        kl = statistics.mean(timed(lambda: gomp.decompress_into(info, d_src, out, ws, args.strategy, stream,
+                                                                phase="lz77"), 10, 3))
+        # algorithmic bytes per launch: decode reads the compressed file and writes the tokens;
+        # LZ77 reads the tokens and writes the output
+        kern = {f"huff_{gomp.huff_variant(info)}_kernel": (kd, C + T),
+                "lz77_batch_kernel" if args.strategy in ("auto", "de") and info.de else "lz77_kernel": (kl, T + U)}
     else:
-        kernels = {"lz77_kernel_ms": round(t_step, 4)}
-
+        kern = {"lz77_batch_kernel (Byte, fused)" if args.strategy in ("auto", "de") and info.de else
+                "lz77_kernel (Byte, fused)": (t_step, C + U)}
+    dom = max(kern, key=lambda k: kern[k][0])
     P, peak_src = peaks()
-    achieved = (U + C) / (t_step * 1e-3) / 1e9
+    kd_ms, kbytes = kern[dom]
+    achieved = kbytes / (kd_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(dom.split(" ")[0], args.config)
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": P, "unit": "GB/s",
-                "frac": round(achieved / P, 4), "traffic": None,
-                "kernel": "whole decompression step (" + ("huff_decode_kernel + lz77_kernel" if info.mode else
-                                                          "lz77_kernel, Byte fused") + ")",
-                "algorithmic_bytes_per_step": U + C, "peak_source": peak_src, **kernels}
+                "frac": round(achieved / P, 4), "traffic": traffic["bytes"] if traffic else None,
+                "kernel": dom, "kernel_ms": round(kd_ms, 4), "algorithmic_bytes_per_launch": kbytes,
+                "traffic_source": traffic["source"] if traffic else None, "peak_source": peak_src,
+                "kernels_ms": {k: round(v[0], 4) for k, v in kern.items()},
+                "step": {"algorithmic_bytes": U + C, "achieved": round((U + C) / (t_step * 1e-3) / 1e9, 2),
+                         "frac": round((U + C) / (t_step * 1e-3) / 1e9 / P, 4)}}
 
     e2e = None
     if not args.no_e2e:

@@ -190,6 +190,23 @@ def _strategy(strategy, stats, phase=None, huff=None):
     return s | (FLAG_STATS if stats else 0)
 
 
+def token_bytes(c):
+    """Bytes of the Bit decoder's token stream for file c (host tensor/array): sum over blocks of 4 B per record
+    + 1 B per literal (FORMAT.md block table; host arithmetic for reporting, no decoding)."""
+    a = np.asarray(c if not isinstance(c, torch.Tensor) else c.cpu().numpy(), dtype=np.uint8)
+    info = get_info(a)
+    t = a[64:64 + 32 * info.n_blocks].view(np.uint32).reshape(-1, 8)
+    return int(4 * t[:, 3].astype(np.int64).sum() + t[:, 4].astype(np.int64).sum())
+
+
+def huff_variant(info):
+    """Which Bit decoder the launcher picks (mirrors decompress_range): "warp" when the mean sub-block holds at
+    least 4 * 32 * 96 bits, else "thread"."""
+    if not info.n_sub_total:
+        return "thread"
+    return "warp" if (info.file_len - info.payload_base) * 8 // info.n_sub_total >= 4 * 32 * 96 else "thread"
+
+
 def decompress_into(info, src, dst, workspace, strategy="auto", stream=None, first_block=0, n_blocks=None,
                     stats=False, phase=None, huff=None):
     """Enqueue gomp_decompress(_blocks) on `stream` (no synchronisation). src/dst/workspace: CUDA uint8

@@ -678,15 +678,6 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       }
     }
     serial = seq_tot != nseq || lit_tot != nl || !tail_ok;
-#ifdef GOMP_DEBUG_GROUP
-    if (b == 0 && k == 0) {
-      uint32_t* dbg = reinterpret_cast<uint32_t*>(a.dst) + vl * 16;
-      dbg[0] = merged; dbg[1] = mpos; dbg[2] = e_rel; dbg[3] = exit_vl; dbg[4] = exit_idx; dbg[5] = lits_t;
-      dbg[6] = nlen_t; dbg[7] = seqs; dbg[8] = seq_inc; dbg[9] = lit_inc; dbg[10] = runin; dbg[11] = serial;
-      dbg[12] = c; dbg[13] = cnt; dbg[14] = lits; dbg[15] = bsz;
-    }
-    return;
-#endif
     if (!serial) {
       // ---------------- pass 2: decode from the true start, write records and literals
       uint32_t ri = seq_inc - seqs, li = lit_inc - lits_t, run2 = runin, bad = 0, maxr = 0;
@@ -1200,11 +1191,15 @@ __device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
 #pragma unroll 1
   for (uint32_t hop = 0; hop < kBW; ++hop) {
     if (q < v.oB) return lds8(v.ring + (q & v.RM));
-    uint32_t h = 0;
+    uint32_t h = 0, ogh = v.og[0];
 #pragma unroll
-    for (uint32_t hh = 1; hh < kBW; ++hh) h = v.og[hh] <= q ? hh : h;
+    for (uint32_t hh = 1; hh < kBW; ++hh) {
+      const bool ge = v.og[hh] <= q;
+      h = ge ? hh : h;
+      ogh = ge ? v.og[hh] : ogh;
+    }
     const uint32_t hs = v.slot0 + h * kSlot;
-    const uint32_t xr = q - v.og[h], y = xr + (v.og[h] & 3u);
+    const uint32_t xr = q - ogh, y = xr + (ogh & 3u);
     const uint32_t bw = lds32(hs + 512 + (y >> 5) * 4), pc = lds32(hs + 512 + kGrpBitWords * 4 + (y >> 5) * 4);
     const uint32_t j = pc + __popc(bw & ((2u << (y & 31)) - 1u)) - 1u;
     const uint4 D = lds128(hs + j * 16);
