@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdint>
 
 #include "format.hpp"
@@ -25,6 +26,9 @@ namespace gomp {
 namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint32_t kPipeStreams = 4;     // compute streams of the pipelined host path
+constexpr uint32_t kPipeMaxChunks = 8;   // chunks of the pipelined host path
+constexpr uint32_t kPipeMinBlocks = 64;  // fewest blocks per chunk
 constexpr int kLz77Warps = 2;        // warps (= data blocks) per CTA of the LZ77 kernel
 constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
 
@@ -1424,9 +1428,11 @@ void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
 }
 
 
+// reset_ws: clear the error word / statistics first (a pipelined caller clears them once); tok_block0: block
+// slot of the workspace token buffer used for block `first` (pipelined chunks in flight use disjoint slots)
 gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
                              size_t src_len, uint8_t* d_dst, size_t dst_cap, void* d_ws, size_t ws_bytes,
-                             int strategy, cudaStream_t st) {
+                             int strategy, cudaStream_t st, bool reset_ws = true, uint32_t tok_block0 = 0) {
   if (!info || !d_src || !d_ws || (!d_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
   if (uint64_t(first) + nblk > info->n_blocks) return GOMP_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(d_src) | reinterpret_cast<uintptr_t>(d_ws)) & 15u) return GOMP_ERR_INVALID_ARG;
@@ -1448,15 +1454,15 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   }
   if (dst_cap < out_bytes) return GOMP_ERR_DST_TOO_SMALL;
   size_t need = 0;
-  gomp_decompress_workspace_size(info, nblk ? nblk : 1, &need);
+  gomp_decompress_workspace_size(info, tok_block0 + (nblk ? nblk : 1), &need);
   if (ws_bytes < need) return GOMP_ERR_WORKSPACE_TOO_SMALL;
-  if (cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  if (reset_ws && cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
   if (nblk == 0) return GOMP_OK;
   Args a{};
   a.src = d_src;
   a.dst = d_dst;
   a.ws = static_cast<uint8_t*>(d_ws);
-  a.tokens = a.ws + kWsHeaderBytes;
+  a.tokens = a.ws + kWsHeaderBytes + uint64_t(tok_block0) * align16(info->max_block_tokens);
   a.total = info->uncompressed_len;
   a.file_len = info->file_len;
   a.payload_base = info->payload_base;
@@ -1554,19 +1560,97 @@ GOMP_EXPORT gomp_status gomp_decompress_blocks(const gomp_info* info, uint32_t f
                           static_cast<cudaStream_t>(stream));
 }
 
+namespace gomp {
+namespace {
+// RAII set of the streams/events of one pipelined host call (destroyed once enqueued work no longer needs
+// them: CUDA releases a destroyed stream/event after its pending work completes)
+struct Pipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr, comp[kPipeStreams] = {};
+  cudaEvent_t ev[2 * kPipeMaxChunks + 2] = {};
+  int nev = 0;
+  bool ok = true;
+  Pipe() {
+    ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& c : comp) ok = ok && cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking) == cudaSuccess;
+  }
+  cudaEvent_t event() {
+    if (nev == int(sizeof(ev) / sizeof(ev[0]))) { ok = false; return nullptr; }
+    if (cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming) != cudaSuccess) { ok = false; return nullptr; }
+    return ev[nev++];
+  }
+  ~Pipe() {
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+    for (auto& c : comp) if (c) cudaStreamDestroy(c);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+  }
+};
+}  // namespace
+}  // namespace gomp
+
+// End-to-end path ("In/Out"): the blocks are cut into up to kPipeMaxChunks chunks; chunk i's
+// compressed bytes go host->device on one copy stream, its kernels run on compute stream i % kPipeStreams once
+// they have arrived, and its output goes device->host on the other copy stream once they are done. Both copy
+// directions and the kernels of different chunks overlap; the caller's stream waits for the last copy.
 GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_t* h_src, size_t src_len, uint8_t* h_dst,
                                              size_t dst_cap, uint8_t* d_src_buf, uint8_t* d_dst_buf, void* d_ws,
                                              size_t ws_bytes, int strategy, void* stream) {
-  if (!info || !h_src || !d_src_buf || (!h_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
+  if (!info || !h_src || !d_src_buf || !d_ws || (!h_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
   if (src_len < info->file_len) return GOMP_ERR_TRUNCATED;
   if (dst_cap < info->uncompressed_len) return GOMP_ERR_DST_TOO_SMALL;
+  size_t need = 0;
+  gomp_decompress_workspace_size(info, 0, &need);
+  if (ws_bytes < need) return GOMP_ERR_WORKSPACE_TOO_SMALL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemcpyAsync(d_src_buf, h_src, info->file_len, cudaMemcpyHostToDevice, st) != cudaSuccess) return GOMP_ERR_CUDA;
-  gomp_status s = decompress_range(info, 0, info->n_blocks, d_src_buf, info->file_len, d_dst_buf,
-                                   info->uncompressed_len, d_ws, ws_bytes, strategy, st);
-  if (s != GOMP_OK) return s;
-  if (info->uncompressed_len &&
-      cudaMemcpyAsync(h_dst, d_dst_buf, info->uncompressed_len, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+  const uint32_t nb = info->n_blocks;
+  const uint64_t flen = info->file_len, bs = info->block_size, U = info->uncompressed_len;
+  // chunking: payloads must be laid out in block order (our compressor does); otherwise one up-front copy
+  const uint64_t tab_end = kHeaderBytes + uint64_t(kBlockEntryBytes) * nb;
+  if (tab_end > flen) return GOMP_ERR_TRUNCATED;
+  uint32_t K = std::min<uint32_t>(kPipeMaxChunks, std::max<uint32_t>(1, (nb + kPipeMinBlocks - 1) / kPipeMinBlocks));
+  std::vector<uint64_t> pend(nb);   // end of block b's payload (+ look-ahead), clamped to the file
+  bool ordered = true;
+  uint64_t prev = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    const uint8_t* te = h_src + kHeaderBytes + uint64_t(kBlockEntryBytes) * b;
+    const uint64_t off = ld64(te), len = ld32(te + 8);
+    ordered = ordered && off >= prev && off <= flen;
+    prev = off;
+    pend[b] = std::min<uint64_t>(flen, off + len + 64);
+  }
+  if (!ordered) K = 1;
+  Pipe p;
+  if (!p.ok) return GOMP_ERR_CUDA;
+  if (cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  cudaEvent_t e0 = p.event();
+  if (!p.ok || cudaEventRecord(e0, st) != cudaSuccess) return GOMP_ERR_CUDA;
+  bool ok = cudaStreamWaitEvent(p.h2d, e0, 0) == cudaSuccess && cudaStreamWaitEvent(p.d2h, e0, 0) == cudaSuccess;
+  for (auto c : p.comp) ok = ok && cudaStreamWaitEvent(c, e0, 0) == cudaSuccess;
+  if (!ok) return GOMP_ERR_CUDA;
+  uint64_t copied = 0;   // bytes [0, copied) of the file are enqueued host->device
+  for (uint32_t i = 0; i < K; ++i) {
+    const uint32_t b0 = uint32_t(uint64_t(nb) * i / K), b1 = uint32_t(uint64_t(nb) * (i + 1) / K);
+    const uint64_t hi = (i + 1 == K || !ordered) ? flen : std::max<uint64_t>(pend[b1 - 1], info->payload_base);
+    if (hi > copied) {
+      if (cudaMemcpyAsync(d_src_buf + copied, h_src + copied, hi - copied, cudaMemcpyHostToDevice, p.h2d) != cudaSuccess)
+        return GOMP_ERR_CUDA;
+      copied = hi;
+    }
+    cudaEvent_t eh = p.event(), ec = p.event();
+    if (!p.ok || cudaEventRecord(eh, p.h2d) != cudaSuccess) return GOMP_ERR_CUDA;
+    cudaStream_t cs = p.comp[i % kPipeStreams];
+    if (cudaStreamWaitEvent(cs, eh, 0) != cudaSuccess) return GOMP_ERR_CUDA;
+    const uint64_t o0 = uint64_t(b0) * bs, o1 = std::min<uint64_t>(uint64_t(b1) * bs, U);
+    const gomp_status s = decompress_range(info, b0, b1 - b0, d_src_buf, flen, d_dst_buf + o0, o1 - o0, d_ws, ws_bytes,
+                                           strategy, cs, false, b0);
+    if (s != GOMP_OK) return s;
+    if (cudaEventRecord(ec, cs) != cudaSuccess || cudaStreamWaitEvent(p.d2h, ec, 0) != cudaSuccess) return GOMP_ERR_CUDA;
+    if (o1 > o0 && cudaMemcpyAsync(h_dst + o0, d_dst_buf + o0, o1 - o0, cudaMemcpyDeviceToHost, p.d2h) != cudaSuccess)
+      return GOMP_ERR_CUDA;
+  }
+  cudaEvent_t ee = p.event();
+  if (!p.ok || cudaEventRecord(ee, p.d2h) != cudaSuccess || cudaStreamWaitEvent(st, ee, 0) != cudaSuccess)
     return GOMP_ERR_CUDA;
   return GOMP_OK;
 }

@@ -210,6 +210,31 @@ def test_host_end_to_end():
         assert np.array_equal(y.numpy(), x)
 
 
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+@pytest.mark.parametrize("n,bs", [(700_001, 16384), (3_000_017, 8192), (100_000, 65536), (0, 65536)])
+def test_host_pipeline(mode, n, bs):
+    """gomp_decompress_host cuts the blocks into up to 8 chunks (>= 64 blocks each) whose copies and kernels
+    overlap on internal streams; output must equal the input, for every chunk count including one."""
+    x = datagen.wiki(n, seed=17)
+    c = gomp.compress(x, mode=mode, block_size=bs).pin_memory()
+    for strategy in ("auto", "mrr"):
+        y = gomp.decompress_host(c, device=DEV, strategy=strategy)
+        assert np.array_equal(y.numpy(), x)
+
+
+def test_host_pipeline_reports_late_error():
+    """A corrupt block in the last chunk of the pipelined host path is reported with its block index."""
+    x = datagen.wiki(3_000_017, seed=18)
+    c = gomp.compress(x, mode="byte", block_size=8192).numpy().copy()
+    info = gomp.get_info(c)
+    b = info.n_blocks - 3
+    off = int(np.frombuffer(c[64 + 32 * b: 72 + 32 * b].tobytes(), dtype=np.uint64)[0])
+    c[off: off + 64] = 0xff                       # first records of block b: lit_len 1023, bad fields
+    with pytest.raises(gomp.GompError) as ei:
+        gomp.decompress_host(torch.from_numpy(c).pin_memory(), device=DEV)
+    assert ei.value.block == b
+
+
 def test_bad_arguments():
     x = datagen.text(10_000)
     c = gomp.compress(x, mode="byte", block_size=4096)
