@@ -1181,7 +1181,9 @@ constexpr uint32_t kBW = 4;                     // warps (groups in flight) per 
 constexpr uint32_t kGrpMaxOut = 4096;           // fast path: group output + start offset within its word
 constexpr uint32_t kLbuf = 1024;                // per-group literal staging buffer (fast path: lit_sum <= 1008)
 constexpr uint32_t kGrpBitWords = kGrpMaxOut / 32;
-constexpr uint32_t kSlot = 512 + 2 * kGrpBitWords * 4 + kLbuf;   // descriptors | bitmap | prefix counts | literals
+// slot: 32 descriptors (16 B) | per output row (32 bytes): sequence-start bitmap word + exclusive prefix count
+// of starts (8 B) | staged literals
+constexpr uint32_t kSlotRows = 512, kSlotLbuf = kSlotRows + kGrpBitWords * 8, kSlot = kSlotLbuf + kLbuf;
 
 __host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kBW * kSlot + kBW * 16 + kBW * 16; }
 
@@ -1204,11 +1206,11 @@ __device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
     }
     const uint32_t hs = v.slot0 + h * kSlot;
     const uint32_t xr = q - ogh, y = xr + (ogh & 3u);
-    const uint32_t bw = lds32(hs + 512 + (y >> 5) * 4), pc = lds32(hs + 512 + kGrpBitWords * 4 + (y >> 5) * 4);
-    const uint32_t j = pc + __popc(bw & ((2u << (y & 31)) - 1u)) - 1u;
+    const uint2 bp = lds64(hs + kSlotRows + (y >> 5) * 8);
+    const uint32_t j = bp.y + __popc(bp.x & ((2u << (y & 31)) - 1u)) - 1u;
     const uint4 D = lds128(hs + j * 16);
-    if (xr < (D.y & 0x7fffffffu)) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.z);
-    if (D.y >> 31) return lds8(hs + 512 + 2 * kGrpBitWords * 4 + xr + D.w);
+    if (xr < (D.y & 0x7fffffffu)) return lds8(hs + kSlotLbuf + xr + D.z);
+    if (D.y >> 31) return lds8(hs + kSlotLbuf + xr + D.w);
     q -= D.w;
   }
   return lds8(v.ring + (q & v.RM));
@@ -1222,10 +1224,10 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
   const uint32_t RING = a.ring_bytes, RM = RING - 1;
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(bz));
   const uint32_t slot0 = ring + RING;
-  const uint32_t prm_s = slot0 + w * kSlot, bits_s = prm_s + 512, pcnt_s = bits_s + kGrpBitWords * 4,
-                 lbuf_s = pcnt_s + kGrpBitWords * 4;
+  const uint32_t prm_s = slot0 + w * kSlot, bits_s = prm_s + kSlotRows, lbuf_s = prm_s + kSlotLbuf;
   const uint32_t tab = slot0 + kBW * kSlot, flg = tab + kBW * 16;
-  sts128(bits_s + lane * 16, make_uint4(0u, 0u, 0u, 0u));          // 128 bitmap words of this warp
+  sts128(bits_s + lane * 32, make_uint4(0u, 0u, 0u, 0u));          // 128 row words of this warp
+  sts128(bits_s + lane * 32 + 16, make_uint4(0u, 0u, 0u, 0u));
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
   const uint8_t* base;
@@ -1307,15 +1309,16 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       const bool own = has && src >= op;
       sts128(prm_s + lane * 16, make_uint4(act ? opr : out_sum, (opr + lit) | (own ? 0x80000000u : 0u), ldl,
                                            own ? ldl - dist : dist));
-      if (act) ats_or(bits_s + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
+      if (act) ats_or(bits_s + ((opr + ob) >> 5) * 8, 1u << ((opr + ob) & 31));
       __syncwarp();
-      // exclusive prefix counts of the bitmap words (lane l: words 4l .. 4l+3)
+      // exclusive prefix counts of the bitmap words (lane l: rows 4l .. 4l+3)
       {
-        const uint4 bw = lds128(bits_s + lane * 16);
-        const uint32_t c0 = __popc(bw.x), c1 = __popc(bw.y), c2 = __popc(bw.z), c3 = __popc(bw.w);
+        const uint4 b01 = lds128(bits_s + lane * 32), b23 = lds128(bits_s + lane * 32 + 16);
+        const uint32_t c0 = __popc(b01.x), c1 = __popc(b01.z), c2 = __popc(b23.x), c3 = __popc(b23.z);
         const uint32_t s4 = c0 + c1 + c2 + c3;
         const uint32_t ex4 = warp_incl_scan_u32(s4, lane) - s4;
-        sts128(pcnt_s + lane * 16, make_uint4(ex4, ex4 + c0, ex4 + c0 + c1, ex4 + c0 + c1 + c2));
+        sts128(bits_s + lane * 32, make_uint4(b01.x, ex4, b01.z, ex4 + c0));
+        sts128(bits_s + lane * 32 + 16, make_uint4(b23.x, ex4 + c0 + c1, b23.z, ex4 + c0 + c1 + c2));
       }
       cp_wait_n<0>();
       __syncthreads();
@@ -1327,26 +1330,23 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
 #pragma unroll
         for (uint32_t rr = 0; rr < 4; ++rr) {
           const uint32_t row = r0 + rr;
-          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
+          const uint32_t x = 32 * row + lane - ob;   // output offset in the group (wraps when before it)
           byte[rr] = 0;
-          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) {
-            const uint32_t bw = lds32(bits_s + row * 4), pc = lds32(pcnt_s + row * 4);
-            const uint32_t j = pc + __popc(bw & le) - 1u;
+          if (x < out_sum) {
+            const uint2 bp = lds64(bits_s + row * 8);
+            const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
             const uint4 D = lds128(prm_s + j * 16);
-            const uint32_t xu = uint32_t(x);
-            if (xu < (D.y & 0x7fffffffu)) byte[rr] = lds8(lbuf_s + xu + D.z);
-            else if (D.y >> 31) byte[rr] = lds8(lbuf_s + xu + D.w);
-            else {
-              const uint32_t q = og + xu - D.w;
-              byte[rr] = q < oB ? lds8(ring + (q & RM)) : chase_byte(bv, q);
-            }
+            // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
+            const bool isl = x < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
+            const uint32_t q = og + x - D.w;
+            const uint32_t sa = inbuf ? lbuf_s + x + (isl ? D.z : D.w) : ring + (q & RM);
+            byte[rr] = (inbuf || q < oB) ? lds8(sa) : chase_byte(bv, q);
           }
         }
 #pragma unroll
         for (uint32_t rr = 0; rr < 4; ++rr) {
-          const uint32_t row = r0 + rr;
-          const int32_t x = int32_t(32 * row + lane) - int32_t(ob);
-          if (row < nrows && x >= 0 && uint32_t(x) < out_sum) sts8(ring + ((og + uint32_t(x)) & RM), byte[rr]);
+          const uint32_t x = 32 * (r0 + rr) + lane - ob;
+          if (x < out_sum) sts8(ring + ((og + x) & RM), byte[rr]);
         }
       }
       if (STATS) {
@@ -1360,7 +1360,8 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
         }
       }
       __syncthreads();
-      sts128(bits_s + lane * 16, make_uint4(0u, 0u, 0u, 0u));
+      sts128(bits_s + lane * 32, make_uint4(0u, 0u, 0u, 0u));
+      sts128(bits_s + lane * 32 + 16, make_uint4(0u, 0u, 0u, 0u));
       // flush completed 16-byte chunks (all warps), at least kFlushBytes at a time
       const uint32_t q1 = (oB + OT) >> 4;
       if (q1 * 16 >= flushed + kFlushBytes) {
@@ -1383,9 +1384,13 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           const uint32_t lit2 = r2 & 1023u, mc2 = (r2 >> 10) & 63u, dist2 = (r2 >> 16) + 1u;
           const uint32_t L2 = mc2 ? mc2 + mm1 : 0u, v2 = lit2 | ((lit2 + L2) << 16);
           const uint32_t inc2 = warp_incl_scan_u32(v2, lane), ex2 = inc2 - v2;
-          const uint32_t op2 = bv.og[ww] + (ex2 >> 16);
-          uint32_t lg2 = lB;
-          for (uint32_t u = 0; u < ww; ++u) lg2 += lds128(tab + u * 16).y;
+          uint32_t og2 = oB, lg2 = lB;
+          for (uint32_t u = 0; u < ww; ++u) {
+            const uint4 tu = lds128(tab + u * 16);
+            og2 += tu.x;
+            lg2 += tu.y;
+          }
+          const uint32_t op2 = og2 + (ex2 >> 16);
           const uint32_t lp2 = lg2 + (ex2 & 0xffffu), dst2 = op2 + lit2;
           if (act2) copy_lits_global(out + op2, lits + lp2, lit2);
           if (!resolve_group<GOMP_STRAT_MRR, STATS>(a, go, lane, act2 && L2, dst2, dst2 - dist2, L2, op2, b, gg * 32))
