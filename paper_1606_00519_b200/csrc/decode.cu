@@ -1169,49 +1169,42 @@ size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * lz_warp_byte
 // ------------------------------------------------------------------ K2b: several warps per data block (DE)
 //
 // One warp per data block (the paper's mapping) leaves a B200 SM with ~7 LZ77 warps at BASELINE C2
-// (1024 blocks), so every group pays the full latency of its dependent chain. Here kBW warps of one CTA take
-// kBW consecutive DE groups of the same block at once (a "batch"). Under the DE rule a group's sources lie
-// below its own start (or in its own literal), but they may lie in an EARLIER group of the same batch, which
-// is being written concurrently: such a byte is resolved by chasing — locate the source position in that
-// group's descriptors (sequence-start bitmap + prefix counts + 16-byte descriptor) and continue from its source
-// (a literal byte, or a position further back) until it lands below the batch start (final in the output ring)
-// or in a literal. Each hop goes to a strictly earlier group, so at most kBW-1 hops. No inter-warp ordering
-// inside a batch; three CTA barriers per batch.
-constexpr uint32_t kBW = 4;                     // warps (groups in flight) per data block
-constexpr uint32_t kGrpMaxOut = 4096;           // fast path: group output + start offset within its word
-constexpr uint32_t kLbuf = 1024;                // per-group literal staging buffer (fast path: lit_sum <= 1008)
-constexpr uint32_t kGrpBitWords = kGrpMaxOut / 32;
-// slot: 32 descriptors (16 B) | per output row (32 bytes): sequence-start bitmap word + exclusive prefix count
-// of starts (8 B) | staged literals
-constexpr uint32_t kSlotRows = 512, kSlotLbuf = kSlotRows + kGrpBitWords * 8, kSlot = kSlotLbuf + kLbuf;
+// (1024 blocks), so every group pays the full latency of its dependent chain. Here the kBW warps of one CTA
+// take kBW consecutive DE groups of the same block at once (a "batch" of up to 128 sequences): warp w reads
+// and scans group B0+w (a5) and writes its sequence descriptors; then the batch output is produced in byte
+// rows of 32 bytes, interleaved over the warps (row r -> warp r % kBW) in steps of kBW rows with a CTA
+// barrier per step, so the warps' work is balanced and every byte before the current step is final in the
+// output ring. A byte is a literal (staged batch literals), an own-literal match byte (ditto) or a match byte
+// whose source is either final (before the step: one ring read) or inside the step: then it is chased —
+// located in the batch descriptors (sequence-start bitmap + prefix counts + 16-byte descriptor) and continued
+// from its own source, strictly backwards, until it is final or a literal.
+constexpr uint32_t kBW = 4;                          // warps (groups in flight) per data block
+constexpr uint32_t kBatchMaxOut = 16384;             // fast path: batch output bytes
+constexpr uint32_t kBatchRows = kBatchMaxOut / 32;
+constexpr uint32_t kBatchLbuf = 4096;                // fast path: batch literal bytes + 16-byte misalignment
+// batch tables after the ring: 128 descriptors | per row: start bitmap word + exclusive start count | literals
+constexpr uint32_t kLzDesc = 0, kLzRows = kBW * 32 * 16, kLzLbuf = kLzRows + kBatchRows * 8,
+                   kLzTab = kLzLbuf + kBatchLbuf, kLzFlg = kLzTab + kBW * 16, kLzEnd = kLzFlg + kBW * 16;
 
-__host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kBW * kSlot + kBW * 16 + kBW * 16; }
+__host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kLzEnd; }
 
 struct BatchView {
-  uint32_t ring, RM, slot0, oB;
-  uint32_t og[kBW];
+  uint32_t ring, RM, desc, rows, lbuf, oB, sB;   // sB: first byte of the current step (absolute in the block)
 };
 
-// value of output byte q (absolute in the block) of the current batch: chase through earlier groups
+// value of byte q (absolute in the block, oB <= sB <= q) of the current step: follow the descriptors back
+// until the byte is a literal or lies before the step
 __device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
 #pragma unroll 1
-  for (uint32_t hop = 0; hop < kBW; ++hop) {
-    if (q < v.oB) return lds8(v.ring + (q & v.RM));
-    uint32_t h = 0, ogh = v.og[0];
-#pragma unroll
-    for (uint32_t hh = 1; hh < kBW; ++hh) {
-      const bool ge = v.og[hh] <= q;
-      h = ge ? hh : h;
-      ogh = ge ? v.og[hh] : ogh;
-    }
-    const uint32_t hs = v.slot0 + h * kSlot;
-    const uint32_t xr = q - ogh, y = xr + (ogh & 3u);
-    const uint2 bp = lds64(hs + kSlotRows + (y >> 5) * 8);
+  for (uint32_t hop = 0; hop < 128; ++hop) {
+    const uint32_t y = q - v.oB;
+    const uint2 bp = lds64(v.rows + (y >> 5) * 8);
     const uint32_t j = bp.y + __popc(bp.x & ((2u << (y & 31)) - 1u)) - 1u;
-    const uint4 D = lds128(hs + j * 16);
-    if (xr < (D.y & 0x7fffffffu)) return lds8(hs + kSlotLbuf + xr + D.z);
-    if (D.y >> 31) return lds8(hs + kSlotLbuf + xr + D.w);
+    const uint4 D = lds128(v.desc + j * 16);
+    if (y < (D.y & 0x7fffffffu)) return lds8(v.lbuf + y + D.z);
+    if (D.y >> 31) return lds8(v.lbuf + y + D.w);
     q -= D.w;
+    if (q < v.sB) break;
   }
   return lds8(v.ring + (q & v.RM));
 }
@@ -1219,15 +1212,13 @@ __device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
 template <bool STATS>
 __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t bz[];
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const uint32_t RING = a.ring_bytes, RM = RING - 1;
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(bz));
-  const uint32_t slot0 = ring + RING;
-  const uint32_t prm_s = slot0 + w * kSlot, bits_s = prm_s + kSlotRows, lbuf_s = prm_s + kSlotLbuf;
-  const uint32_t tab = slot0 + kBW * kSlot, flg = tab + kBW * 16;
-  sts128(bits_s + lane * 32, make_uint4(0u, 0u, 0u, 0u));          // 128 row words of this warp
-  sts128(bits_s + lane * 32 + 16, make_uint4(0u, 0u, 0u, 0u));
+  const uint32_t desc_s = ring + RING + kLzDesc, rows_s = ring + RING + kLzRows, lbuf_s = ring + RING + kLzLbuf;
+  const uint32_t tab = ring + RING + kLzTab, flg = ring + RING + kLzFlg;
+  for (uint32_t r = threadIdx.x; r < kBatchRows / 2; r += 32 * kBW) sts128(rows_s + r * 16, make_uint4(0u, 0u, 0u, 0u));
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
   const uint8_t* base;
@@ -1264,19 +1255,18 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     const uint32_t tot = __shfl_sync(FULL, incl, 31);
     const uint32_t ex = incl - v;
     const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
-    if (lane == 0) sts128(tab + w * 16, make_uint4(out_sum, lit_sum, 0u, 0u));
+    const uint32_t ne = __ballot_sync(FULL, act && lit + L != 0);   // non-empty sequences (own a start bit)
+    if (lane == 0) sts128(tab + w * 16, make_uint4(out_sum, lit_sum, __popc(ne), 0u));
     __syncthreads();
-    // batch offsets of every group (all warps compute all of them)
-    BatchView bv;
-    bv.ring = ring; bv.RM = RM; bv.slot0 = slot0; bv.oB = oB;
-    uint32_t og = oB, lg = lB, OT = 0, LT = 0;
+    // batch offsets (all warps compute all of them)
+    uint32_t og = oB, lg = lB, dbase = 0, OT = 0, LT = 0, NT = 0;
 #pragma unroll
     for (uint32_t ww = 0; ww < kBW; ++ww) {
       const uint4 t = lds128(tab + ww * 16);
-      bv.og[ww] = oB + OT;
-      if (ww == w) { og = oB + OT; lg = lB + LT; }
+      if (ww == w) { og = oB + OT; lg = lB + LT; dbase = NT; }
       OT += t.x;
       LT += t.y;
+      NT += t.z;
     }
     const uint32_t op = og + (ex >> 16), lp = lg + (ex & 0xffffu), dst = op + lit, src = dst - dist;
     const bool has = act && L;
@@ -1285,69 +1275,70 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     const bool bad_sz = og + out_sum > ulen || lg + lit_sum > e.n_lit;
     const bool any_rec = __any_sync(FULL, bad_rec), any_ref = __any_sync(FULL, bad_ref);
     const bool de_ok = __all_sync(FULL, !has || src + L <= og || src >= op);
-    const bool fast_g = de_ok && (og & 3u) + out_sum <= kGrpMaxOut && lit_sum + 16 <= kLbuf;
     if (lane == 0) {
       if (any_ref || any_rec || bad_sz)
         report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
-      sts32(flg + w * 4, ((any_ref || any_rec || bad_sz) ? 1u : 0u) | (fast_g ? 0u : 2u) | (de_ok ? 0u : 4u));
+      sts32(flg + w * 4, ((any_ref || any_rec || bad_sz) ? 1u : 0u) | (de_ok ? 0u : 6u));
     }
     __syncthreads();
     uint32_t fl = 0;
 #pragma unroll
     for (uint32_t ww = 0; ww < kBW; ++ww) fl |= lds32(flg + ww * 4);
     if (fl & 1u) return;                                       // device error already reported
-    const bool batch_fast = !(fl & 2u) && OT + a.window + 16 <= RING && oB + OT - flushed <= RING;
+    const bool batch_fast = !(fl & 2u) && OT <= kBatchMaxOut && LT + 32 <= kBatchLbuf && OT + a.window + 16 <= RING &&
+                            oB + OT - flushed <= RING;
     if (batch_fast) {
-      // stage this group's literal bytes [lg, lg + lit_sum) (16-byte chunks) into its literal buffer
-      const uint8_t* la = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits + lg) & ~uintptr_t(15));
-      const uint32_t lofs = uint32_t((lits + lg) - la), nch = (lofs + lit_sum + 15) / 16;
-      for (uint32_t c = lane; c < nch; c += 32) cp_async16(lbuf_s + 16 * c, la + 16 * c);
+      // stage the batch's literal bytes [lB, lB + LT) (16-byte chunks) into the literal buffer
+      const uint8_t* la = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits + lB) & ~uintptr_t(15));
+      const uint32_t lofs = uint32_t((lits + lB) - la), nch = (lofs + LT + 15) / 16;
+      for (uint32_t c = threadIdx.x; c < nch; c += 32 * kBW) cp_async16(lbuf_s + 16 * c, la + 16 * c);
       cp_commit();
-      // descriptors: start, literal end | own << 31, literal delta, match delta (own: lbuf, else distance)
-      const uint32_t opr = ex >> 16, ob = og & 3u;
-      const uint32_t ldl = lofs + (ex & 0xffffu) - opr;
+      // descriptors (batch-relative): start, literal end | own << 31, literal delta, match delta (own: literal
+      // buffer, else the distance); one start bit per non-empty sequence
+      const uint32_t y0 = op - oB, ldl = lp - lB + lofs - y0;
       const bool own = has && src >= op;
-      sts128(prm_s + lane * 16, make_uint4(act ? opr : out_sum, (opr + lit) | (own ? 0x80000000u : 0u), ldl,
-                                           own ? ldl - dist : dist));
-      if (act) ats_or(bits_s + ((opr + ob) >> 5) * 8, 1u << ((opr + ob) & 31));
-      __syncwarp();
-      // exclusive prefix counts of the bitmap words (lane l: rows 4l .. 4l+3)
-      {
-        const uint4 b01 = lds128(bits_s + lane * 32), b23 = lds128(bits_s + lane * 32 + 16);
-        const uint32_t c0 = __popc(b01.x), c1 = __popc(b01.z), c2 = __popc(b23.x), c3 = __popc(b23.z);
-        const uint32_t s4 = c0 + c1 + c2 + c3;
-        const uint32_t ex4 = warp_incl_scan_u32(s4, lane) - s4;
-        sts128(bits_s + lane * 32, make_uint4(b01.x, ex4, b01.z, ex4 + c0));
-        sts128(bits_s + lane * 32 + 16, make_uint4(b23.x, ex4 + c0 + c1, b23.z, ex4 + c0 + c1 + c2));
+      if ((ne >> lane) & 1u) {
+        sts128(desc_s + (dbase + __popc(ne & lt)) * 16,
+               make_uint4(y0, (y0 + lit) | (own ? 0x80000000u : 0u), ldl, own ? ldl - dist : dist));
+        ats_or(rows_s + (y0 >> 5) * 8, 1u << (y0 & 31));
       }
       cp_wait_n<0>();
       __syncthreads();
-      // a6 + a7: byte rows of this group (rows aligned to the bitmap words: y = x + ob)
-      const uint32_t nrows = (ob + out_sum + 31) / 32;
-      const uint32_t le = (2u << lane) - 1u;
-      for (uint32_t r0 = 0; r0 < nrows; r0 += 4) {
-        uint32_t byte[4];
-#pragma unroll
-        for (uint32_t rr = 0; rr < 4; ++rr) {
-          const uint32_t row = r0 + rr;
-          const uint32_t x = 32 * row + lane - ob;   // output offset in the group (wraps when before it)
-          byte[rr] = 0;
-          if (x < out_sum) {
-            const uint2 bp = lds64(bits_s + row * 8);
-            const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
-            const uint4 D = lds128(prm_s + j * 16);
-            // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
-            const bool isl = x < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
-            const uint32_t q = og + x - D.w;
-            const uint32_t sa = inbuf ? lbuf_s + x + (isl ? D.z : D.w) : ring + (q & RM);
-            byte[rr] = (inbuf || q < oB) ? lds8(sa) : chase_byte(bv, q);
+      // exclusive prefix counts of the start bits per row (warp 0; lane l: rows 16l .. 16l+15)
+      const uint32_t nrows = (OT + 31) / 32;
+      if (w == 0) {
+        uint32_t cnt = 0;
+        for (uint32_t k = 0; k < 16; ++k) {
+          const uint32_t row = lane * 16 + k;
+          if (row < nrows) cnt += __popc(lds32(rows_s + row * 8));
+        }
+        uint32_t pre = warp_incl_scan_u32(cnt, lane) - cnt;
+        for (uint32_t k = 0; k < 16; ++k) {
+          const uint32_t row = lane * 16 + k;
+          if (row < nrows) {
+            const uint32_t bw = lds32(rows_s + row * 8);
+            sts32(rows_s + row * 8 + 4, pre);
+            pre += __popc(bw);
           }
         }
-#pragma unroll
-        for (uint32_t rr = 0; rr < 4; ++rr) {
-          const uint32_t x = 32 * (r0 + rr) + lane - ob;
-          if (x < out_sum) sts8(ring + ((og + x) & RM), byte[rr]);
+      }
+      __syncthreads();
+      // a6 + a7: the batch's byte rows, kBW rows per step (row r by warp r % kBW), a CTA barrier per step
+      BatchView bv{ring, RM, desc_s, rows_s, lbuf_s, oB, oB};
+      for (uint32_t s0 = 0; s0 < nrows; s0 += kBW) {
+        const uint32_t row = s0 + w, y = row * 32 + lane;
+        bv.sB = oB + s0 * 32;
+        if (y < OT) {
+          const uint2 bp = lds64(rows_s + row * 8);
+          const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
+          const uint4 D = lds128(desc_s + j * 16);
+          // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
+          const bool isl = y < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
+          const uint32_t q = oB + y - D.w;
+          const uint32_t sa = inbuf ? lbuf_s + y + (isl ? D.z : D.w) : ring + (q & RM);
+          sts8(ring + ((oB + y) & RM), (inbuf || q < bv.sB) ? lds8(sa) : chase_byte(bv, q));
         }
+        __syncthreads();
       }
       if (STATS) {
         const uint32_t any = __ballot_sync(FULL, has);
@@ -1359,9 +1350,7 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
         }
       }
-      __syncthreads();
-      sts128(bits_s + lane * 32, make_uint4(0u, 0u, 0u, 0u));
-      sts128(bits_s + lane * 32 + 16, make_uint4(0u, 0u, 0u, 0u));
+      for (uint32_t row = threadIdx.x; row < nrows; row += 32 * kBW) sts32(rows_s + row * 8, 0u);
       // flush completed 16-byte chunks (all warps), at least kFlushBytes at a time
       const uint32_t q1 = (oB + OT) >> 4;
       if (q1 * 16 >= flushed + kFlushBytes) {
@@ -1370,11 +1359,12 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
         flushed = q1 * 16;
       }
     } else {
-      // slow batch (a group too large for the buffers, or not DE): flush the ring, then warp 0 runs the groups
-      // of the batch one by one in global memory with MRR (exact for any valid file), then reload the window
+      // slow batch (too large for the buffers, or not DE): flush the ring, then warp 0 runs the groups of the
+      // batch one by one in global memory with MRR (exact for any valid file), then reload the window
       for (uint32_t p = flushed + threadIdx.x; p < oB; p += 32 * kBW) out[p] = uint8_t(lds8(ring + (p & RM)));
       __syncthreads();
       if (w == 0) {
+        uint32_t og2 = oB, lg2 = lB;
         for (uint32_t ww = 0; ww < kBW; ++ww) {
           const uint32_t gg = B0 + ww, ii = gg * 32 + lane;
           if (gg >= ngroups) break;
@@ -1384,18 +1374,14 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           const uint32_t lit2 = r2 & 1023u, mc2 = (r2 >> 10) & 63u, dist2 = (r2 >> 16) + 1u;
           const uint32_t L2 = mc2 ? mc2 + mm1 : 0u, v2 = lit2 | ((lit2 + L2) << 16);
           const uint32_t inc2 = warp_incl_scan_u32(v2, lane), ex2 = inc2 - v2;
-          uint32_t og2 = oB, lg2 = lB;
-          for (uint32_t u = 0; u < ww; ++u) {
-            const uint4 tu = lds128(tab + u * 16);
-            og2 += tu.x;
-            lg2 += tu.y;
-          }
-          const uint32_t op2 = og2 + (ex2 >> 16);
-          const uint32_t lp2 = lg2 + (ex2 & 0xffffu), dst2 = op2 + lit2;
+          const uint32_t op2 = og2 + (ex2 >> 16), lp2 = lg2 + (ex2 & 0xffffu), dst2 = op2 + lit2;
           if (act2) copy_lits_global(out + op2, lits + lp2, lit2);
           if (!resolve_group<GOMP_STRAT_MRR, STATS>(a, go, lane, act2 && L2, dst2, dst2 - dist2, L2, op2, b, gg * 32))
             break;
           __syncwarp();
+          const uint4 tu = lds128(tab + ww * 16);
+          og2 += tu.x;
+          lg2 += tu.y;
         }
       }
       __syncthreads();
@@ -1418,6 +1404,7 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
   for (uint32_t p = max(q1 * 16, flushed) + threadIdx.x; p < oB; p += 32 * kBW) out[p] = uint8_t(lds8(ring + (p & RM)));
 }
+
 
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
