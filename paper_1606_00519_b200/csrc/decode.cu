@@ -1294,35 +1294,20 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       for (uint32_t c = threadIdx.x; c < nch; c += 32 * kBW) cp_async16(lbuf_s + 16 * c, la + 16 * c);
       cp_commit();
       // descriptors (batch-relative): start, literal end | own << 31, literal delta, match delta (own: literal
-      // buffer, else the distance); one start bit per non-empty sequence
-      const uint32_t y0 = op - oB, ldl = lp - lB + lofs - y0;
+      // buffer, else the distance); one start bit per non-empty sequence; and per row r >= 1 the number of
+      // sequences starting before it (written by the sequence holding byte 32r - 1)
+      const uint32_t y0 = op - oB, y1 = y0 + lit + L, ldl = lp - lB + lofs - y0;
       const bool own = has && src >= op;
       if ((ne >> lane) & 1u) {
-        sts128(desc_s + (dbase + __popc(ne & lt)) * 16,
-               make_uint4(y0, (y0 + lit) | (own ? 0x80000000u : 0u), ldl, own ? ldl - dist : dist));
+        const uint32_t jj = dbase + __popc(ne & lt);
+        sts128(desc_s + jj * 16, make_uint4(y0, (y0 + lit) | (own ? 0x80000000u : 0u), ldl, own ? ldl - dist : dist));
         ats_or(rows_s + (y0 >> 5) * 8, 1u << (y0 & 31));
+        for (uint32_t rr = (y0 + 32) >> 5; rr <= (y1 >> 5) && rr * 32 < OT; ++rr) sts32(rows_s + rr * 8 + 4, jj + 1);
       }
+      if (threadIdx.x == 0) sts32(rows_s + 4, 0u);
       cp_wait_n<0>();
       __syncthreads();
-      // exclusive prefix counts of the start bits per row (warp 0; lane l: rows 16l .. 16l+15)
       const uint32_t nrows = (OT + 31) / 32;
-      if (w == 0) {
-        uint32_t cnt = 0;
-        for (uint32_t k = 0; k < 16; ++k) {
-          const uint32_t row = lane * 16 + k;
-          if (row < nrows) cnt += __popc(lds32(rows_s + row * 8));
-        }
-        uint32_t pre = warp_incl_scan_u32(cnt, lane) - cnt;
-        for (uint32_t k = 0; k < 16; ++k) {
-          const uint32_t row = lane * 16 + k;
-          if (row < nrows) {
-            const uint32_t bw = lds32(rows_s + row * 8);
-            sts32(rows_s + row * 8 + 4, pre);
-            pre += __popc(bw);
-          }
-        }
-      }
-      __syncthreads();
       // a6 + a7: the batch's byte rows, kBW rows per step (row r by warp r % kBW), a CTA barrier per step
       BatchView bv{ring, RM, desc_s, rows_s, lbuf_s, oB, oB};
       for (uint32_t s0 = 0; s0 < nrows; s0 += kBW) {
