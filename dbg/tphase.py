@@ -1,0 +1,20 @@
+import sys, statistics
+sys.path.insert(0, '.')
+import torch, datagen, paper_1606_00519_b200 as gomp
+if len(sys.argv) > 2: gomp.LIB_PATH = sys.argv[2]
+phase = sys.argv[1]
+x = datagen.wiki(256 << 20, seed=2)
+c = gomp.compress(x, mode="bit", de=True, block_size=262144, sub_blocks_per_block=16)
+info = gomp.get_info(c)
+d = c.cuda(); out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device="cuda")
+ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device="cuda")
+gomp.decompress_into(info, d, out, ws, phase="decode")
+ph = None if phase == "all" else phase
+for _ in range(3): gomp.decompress_into(info, d, out, ws, phase=ph)
+ts = []
+for _ in range(10):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); gomp.decompress_into(info, d, out, ws, phase=ph); b.record(); torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b))
+ok = torch.equal(out.cpu(), torch.from_numpy(x)) if ph is None else None
+print(sys.argv[1:], "ms", round(statistics.mean(ts), 4), "ok", ok)

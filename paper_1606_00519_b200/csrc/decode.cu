@@ -1180,6 +1180,7 @@ size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * lz_warp_byte
 // from its own source, strictly backwards, until it is final or a literal.
 constexpr uint32_t kBW = 4;                          // warps (groups in flight) per data block
 constexpr uint32_t kBatchMaxOut = 16384;             // fast path: batch output bytes
+constexpr uint32_t kLzRPS = 2;                       // rows per warp per barrier step
 constexpr uint32_t kBatchRows = kBatchMaxOut / 32;
 constexpr uint32_t kBatchLbuf = 4096;                // fast path: batch literal bytes + 16-byte misalignment
 // batch tables after the ring: 128 descriptors | per row: start bitmap word + exclusive start count | literals
@@ -1310,18 +1311,28 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       const uint32_t nrows = (OT + 31) / 32;
       // a6 + a7: the batch's byte rows, kBW rows per step (row r by warp r % kBW), a CTA barrier per step
       BatchView bv{ring, RM, desc_s, rows_s, lbuf_s, oB, oB};
-      for (uint32_t s0 = 0; s0 < nrows; s0 += kBW) {
-        const uint32_t row = s0 + w, y = row * 32 + lane;
+      for (uint32_t s0 = 0; s0 < nrows; s0 += kBW * kLzRPS) {
         bv.sB = oB + s0 * 32;
-        if (y < OT) {
-          const uint2 bp = lds64(rows_s + row * 8);
-          const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
-          const uint4 D = lds128(desc_s + j * 16);
-          // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
-          const bool isl = y < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
-          const uint32_t q = oB + y - D.w;
-          const uint32_t sa = inbuf ? lbuf_s + y + (isl ? D.z : D.w) : ring + (q & RM);
-          sts8(ring + ((oB + y) & RM), (inbuf || q < bv.sB) ? lds8(sa) : chase_byte(bv, q));
+        uint32_t val[kLzRPS];
+#pragma unroll
+        for (uint32_t k = 0; k < kLzRPS; ++k) {
+          const uint32_t row = s0 + w + kBW * k, y = row * 32 + lane;
+          val[k] = 0;
+          if (y < OT) {
+            const uint2 bp = lds64(rows_s + row * 8);
+            const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
+            const uint4 D = lds128(desc_s + j * 16);
+            // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
+            const bool isl = y < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
+            const uint32_t q = oB + y - D.w;
+            const uint32_t sa = inbuf ? lbuf_s + y + (isl ? D.z : D.w) : ring + (q & RM);
+            val[k] = (inbuf || q < bv.sB) ? lds8(sa) : chase_byte(bv, q);
+          }
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kLzRPS; ++k) {
+          const uint32_t y = (s0 + w + kBW * k) * 32 + lane;
+          if (y < OT) sts8(ring + ((oB + y) & RM), val[k]);
         }
         __syncthreads();
       }
