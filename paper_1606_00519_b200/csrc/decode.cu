@@ -1170,56 +1170,79 @@ size_t lz77_smem_bytes(uint32_t ring) { return size_t(kLz77Warps) * lz_warp_byte
 //
 // One warp per data block (the paper's mapping) leaves a B200 SM with ~7 LZ77 warps at BASELINE C2
 // (1024 blocks), so every group pays the full latency of its dependent chain. Here the kBW warps of one CTA
-// take kBW consecutive DE groups of the same block at once (a "batch" of up to 128 sequences): warp w reads
-// and scans group B0+w (a5) and writes its sequence descriptors; then the batch output is produced in byte
-// rows of 32 bytes, interleaved over the warps (row r -> warp r % kBW) in steps of kBW rows with a CTA
-// barrier per step, so the warps' work is balanced and every byte before the current step is final in the
-// output ring. A byte is a literal (staged batch literals), an own-literal match byte (ditto) or a match byte
-// whose source is either final (before the step: one ring read) or inside the step: then it is chased —
-// located in the batch descriptors (sequence-start bitmap + prefix counts + 16-byte descriptor) and continued
-// from its own source, strictly backwards, until it is final or a literal.
-constexpr uint32_t kBW = 4;                          // warps (groups in flight) per data block
-constexpr uint32_t kBatchMaxOut = 16384;             // fast path: batch output bytes
-constexpr uint32_t kLzRPS = 2;                       // rows per warp per barrier step
-constexpr uint32_t kBatchRows = kBatchMaxOut / 32;
-constexpr uint32_t kBatchLbuf = 4096;                // fast path: batch literal bytes + 16-byte misalignment
-// batch tables after the ring: 128 descriptors | per row: start bitmap word + exclusive start count | literals
-constexpr uint32_t kLzDesc = 0, kLzRows = kBW * 32 * 16, kLzLbuf = kLzRows + kBatchRows * 8,
-                   kLzTab = kLzLbuf + kBatchLbuf, kLzFlg = kLzTab + kBW * 16, kLzEnd = kLzFlg + kBW * 16;
+// take kBW consecutive DE groups of the same block at once (a "batch" of up to 32·kBW sequences). Each warp
+// runs the paper's per-group steps on its group with one sequence per lane: a5 record + one packed
+// exclusive scan, then the batch offsets from the kBW group totals; a6 every lane copies its literal string
+// from the staged literal ring into the output ring; a7 every lane copies its back-reference inside the output
+// ring, in one round (DE). Under DE a group's sources lie below the group's start or in the lane's
+// own literal string, so a warp only has to wait for the earlier warps of its batch when one of its sources
+// reaches into the batch (a chain of named barriers; no wait otherwise). Copies are 32-bit word copies with
+// funnel shifts (no overlap: reading R2). Literal bytes are prefetched by cp.async (LDGSTS) in 2 KiB units
+// into an 8 KiB literal ring well ahead of use; completed output is flushed with coalesced 16-byte stores.
+constexpr uint32_t kBW = 4;                 // warps (groups in flight) per data block
+constexpr uint32_t kLzLR = 8192;            // literal ring bytes
+constexpr uint32_t kLzLUnit = 32 * kBW * 16;  // literal prefetch unit: one 16-byte cp.async per thread
+constexpr uint32_t kLzBatchMaxOut = 4096;   // fast path: batch output bytes = zero-ahead distance
+constexpr uint32_t kLzFlush = 4096;         // ring -> HBM flush granularity
+// batch tables after the ring: literal ring | per-warp group totals (u32 each) | per-warp flags
+constexpr uint32_t kLzTab = kLzLR, kLzFlg = kLzTab + 16, kLzEnd = kLzFlg + kBW * 4;
 
 __host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kLzEnd; }
 
-struct BatchView {
-  uint32_t ring, RM, desc, rows, lbuf, oB, sB;   // sB: first byte of the current step (absolute in the block)
-};
+// named barriers 1..3 between consecutive warps (immediate ids: ptxas then reserves only those)
+__device__ __forceinline__ void chain_sync(uint32_t id) {
+  if (id == 1) asm volatile("bar.sync 1, 64;" ::: "memory");
+  else if (id == 2) asm volatile("bar.sync 2, 64;" ::: "memory");
+  else asm volatile("bar.sync 3, 64;" ::: "memory");
+}
+__device__ __forceinline__ void chain_arrive(uint32_t id) {
+  if (id == 1) asm volatile("bar.arrive 1, 64;" ::: "memory");
+  else if (id == 2) asm volatile("bar.arrive 2, 64;" ::: "memory");
+  else asm volatile("bar.arrive 3, 64;" ::: "memory");
+}
+static_assert(kBW <= 4, "chain barriers 1..3");
 
-// value of byte q (absolute in the block, oB <= sB <= q) of the current step: follow the descriptors back
-// until the byte is a literal or lies before the step
-__device__ __forceinline__ uint32_t chase_byte(const BatchView& v, uint32_t q) {
-#pragma unroll 1
-  for (uint32_t hop = 0; hop < 128; ++hop) {
-    const uint32_t y = q - v.oB;
-    const uint2 bp = lds64(v.rows + (y >> 5) * 8);
-    const uint32_t j = bp.y + __popc(bp.x & ((2u << (y & 31)) - 1u)) - 1u;
-    const uint4 D = lds128(v.desc + j * 16);
-    if (y < (D.y & 0x7fffffffu)) return lds8(v.lbuf + y + D.z);
-    if (D.y >> 31) return lds8(v.lbuf + y + D.w);
-    q -= D.w;
-    if (q < v.sB) break;
+// Copy n >= 1 bytes from power-of-two shared ring S (mask sm) position s to the output ring D (mask dm) position
+// d; the ranges do not overlap (dist >= L, reading R2). The destination range of the current batch is zero
+// beforehand (zero-ahead frontier), so the two partial words at its ends are OR-ed in (RED.OR; a neighbouring
+// lane may own the other bytes) and every word in between is a plain store: no byte loops. Source word k of the
+// destination word at p is the funnel shift of the two source words around p + (s - d); bytes of a source word
+// outside [s, s+n) are discarded by the masks.
+__device__ __forceinline__ void or_copy(uint32_t D, uint32_t dm, uint32_t d, uint32_t S, uint32_t sm, uint32_t s,
+                                        uint32_t n) {
+  const uint32_t e = d + n, last = (e - 1) & ~3u, sh = ((s - d) & 3u) * 8u;
+  uint32_t p = d & ~3u, sa = (s - (d & 3u)) & ~3u;
+  uint32_t lo = ldsw(S + (sa & sm)), hi = ldsw(S + ((sa + 4) & sm));
+  const uint32_t mlast = 0xffffffffu >> ((3u - ((e - 1) & 3u)) * 8u);
+  uint32_t m = 0xffffffffu << ((d & 3u) * 8u);
+  if (p == last) m &= mlast;
+  ats_or(D + (p & dm), __funnelshift_r(lo, hi, sh) & m);
+  p += 4; sa += 4; lo = hi;
+  for (; p + 16 <= last; p += 16) {
+    const uint32_t w1 = ldsw(S + ((sa + 4) & sm)), w2 = ldsw(S + ((sa + 8) & sm)), w3 = ldsw(S + ((sa + 12) & sm)),
+                   w4 = ldsw(S + ((sa + 16) & sm));
+    sts32(D + (p & dm), __funnelshift_r(lo, w1, sh));
+    sts32(D + ((p + 4) & dm), __funnelshift_r(w1, w2, sh));
+    sts32(D + ((p + 8) & dm), __funnelshift_r(w2, w3, sh));
+    sts32(D + ((p + 12) & dm), __funnelshift_r(w3, w4, sh));
+    lo = w4; sa += 16;
   }
-  return lds8(v.ring + (q & v.RM));
+  for (; p < last; p += 4) {
+    hi = ldsw(S + ((sa + 4) & sm));
+    sts32(D + (p & dm), __funnelshift_r(lo, hi, sh));
+    lo = hi; sa += 4;
+  }
+  if (p == last) ats_or(D + (p & dm), __funnelshift_r(lo, ldsw(S + ((sa + 4) & sm)), sh) & mlast);
 }
 
 template <bool STATS>
 __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t bz[];
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
-  const uint32_t RING = a.ring_bytes, RM = RING - 1;
+  const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLzLR - 1;
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(bz));
-  const uint32_t desc_s = ring + RING + kLzDesc, rows_s = ring + RING + kLzRows, lbuf_s = ring + RING + kLzLbuf;
-  const uint32_t tab = ring + RING + kLzTab, flg = ring + RING + kLzFlg;
-  for (uint32_t r = threadIdx.x; r < kBatchRows / 2; r += 32 * kBW) sts128(rows_s + r * 16, make_uint4(0u, 0u, 0u, 0u));
+  const uint32_t lring = ring + RING, tab = ring + RING + kLzTab, flg = ring + RING + kLzFlg;
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
   const uint8_t* base;
@@ -1237,17 +1260,37 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
   }
   const uint32_t* recs = reinterpret_cast<const uint32_t*>(base);
   const uint8_t* lits = base + 4ull * e.n_seq;
+  // literal stream staging: rel position = byte offset from the 16-aligned address below the stream
+  const uint8_t* lal = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits) & ~uintptr_t(15));
+  const uint32_t lofs = uint32_t(lits - lal), lend16 = (lofs + e.n_lit + 15u) & ~15u;
+  uint32_t lf = 0;        // rel literal bytes issued to the literal ring (multiple of kLzLUnit)
+  uint32_t lB_prev = 0;   // literal start of the previous batch: bytes below it are consumed
   uint8_t* out = a.dst + uint64_t(bi) * a.block_size;
   const uint32_t mm1 = a.min_match - 1, n_seq = e.n_seq, ngroups = (n_seq + 31) / 32;
   const GlobalOut go{out};
   uint32_t oB = 0, lB = 0, flushed = 0;
-  uint32_t r_next = (w * 32 + lane) < n_seq ? __ldg(recs + w * 32 + lane) : 0u;
-  __syncthreads();
-  for (uint32_t B0 = 0; B0 < ngroups; B0 += kBW) {
-    const uint32_t g = B0 + w, i = g * 32 + lane;
+  uint32_t i = w * 32 + lane;                                   // this lane's sequence in the current batch
+  const uint32_t* rp = recs + i;
+  uint32_t r_next = i < n_seq ? __ldg(rp) : 0u;
+  // zero-ahead frontier (16-aligned): ring bytes [oB, zf) are zero before a batch writes them (or_copy), and
+  // zf >= oB + kLzBatchMaxOut
+  uint32_t zf = kLzBatchMaxOut;
+  for (uint32_t p = 16 * threadIdx.x; p < zf; p += 16 * 32 * kBW) sts128(ring + p, make_uint4(0u, 0u, 0u, 0u));
+  for (uint32_t B0 = 0; B0 < ngroups; B0 += kBW, i += 32 * kBW) {
+    const uint32_t g = B0 + w;
     const bool act = i < n_seq;
     const uint32_t r = r_next;
-    r_next = (i + 32 * kBW) < n_seq ? __ldg(recs + i + 32 * kBW) : 0u;
+    rp += 32 * kBW;
+    r_next = (i + 32 * kBW) < n_seq ? __ldg(rp) : 0u;
+    // literal prefetch: units up to (previous batch start + ring) may be issued (earlier bytes are consumed);
+    // all but the two most recent units have landed after the wait (published by the barrier below)
+    while (lf < lend16 && lf + kLzLUnit <= lofs + lB_prev + kLzLR) {
+      const uint32_t off = lf + threadIdx.x * 16;
+      if (off < lend16) cp_async16(lring + (off & LM), lal + off);
+      cp_commit();
+      lf += kLzLUnit;
+    }
+    cp_wait_n<2>();
     // a5: record decode + packed scan of this warp's group
     const uint32_t lit = r & 1023u, mcode = (r >> 10) & 63u, dist = (r >> 16) + 1u;
     const uint32_t L = mcode ? mcode + mm1 : 0u;
@@ -1255,87 +1298,70 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     const uint32_t incl = warp_incl_scan_u32(v, lane);
     const uint32_t tot = __shfl_sync(FULL, incl, 31);
     const uint32_t ex = incl - v;
-    const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
-    const uint32_t ne = __ballot_sync(FULL, act && lit + L != 0);   // non-empty sequences (own a start bit)
-    if (lane == 0) sts128(tab + w * 16, make_uint4(out_sum, lit_sum, __popc(ne), 0u));
+    if (lane == 0) sts32(tab + w * 4, tot);
     __syncthreads();
-    // batch offsets (all warps compute all of them)
-    uint32_t og = oB, lg = lB, dbase = 0, OT = 0, LT = 0, NT = 0;
-#pragma unroll
-    for (uint32_t ww = 0; ww < kBW; ++ww) {
-      const uint4 t = lds128(tab + ww * 16);
-      if (ww == w) { og = oB + OT; lg = lB + LT; dbase = NT; }
-      OT += t.x;
-      LT += t.y;
-      NT += t.z;
+    // flush the completed output of earlier batches (final after the barrier), at least kFlushBytes at a time
+    if (oB >= flushed + kLzFlush + 16) {
+      const uint32_t q1 = oB >> 4;
+      for (uint32_t q = (flushed >> 4) + threadIdx.x; q < q1; q += 32 * kBW)
+        reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
+      flushed = q1 * 16;
     }
+    // batch offsets (all warps compute all of them); group totals are (out << 16 | lit), each half < 2^16
+    const uint4 T4 = lds128(tab);
+    static_assert(kBW == 4, "batch offsets from one 16-byte load");
+    const uint32_t o0 = T4.x >> 16, o1 = T4.y >> 16, o2 = T4.z >> 16, o3 = T4.w >> 16;
+    const uint32_t l0 = T4.x & 0xffffu, l1 = T4.y & 0xffffu, l2 = T4.z & 0xffffu, l3 = T4.w & 0xffffu;
+    const uint32_t OT = o0 + o1 + o2 + o3, LT = l0 + l1 + l2 + l3;
+    const uint32_t ob_w = w == 0 ? 0u : w == 1 ? o0 : w == 2 ? o0 + o1 : o0 + o1 + o2;
+    const uint32_t lb_w = w == 0 ? 0u : w == 1 ? l0 : w == 2 ? l0 + l1 : l0 + l1 + l2;
+    const uint32_t og = oB + ob_w, lg = lB + lb_w;
+    const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
     const uint32_t op = og + (ex >> 16), lp = lg + (ex & 0xffffu), dst = op + lit, src = dst - dist;
     const bool has = act && L;
-    const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst);
-    const bool bad_rec = act && !mcode && (r >> 16);
+    const bool bad_lane = act && (L ? (dist < L || dist > a.window || dist > dst) : (r >> 16) != 0);
     const bool bad_sz = og + out_sum > ulen || lg + lit_sum > e.n_lit;
-    const bool any_rec = __any_sync(FULL, bad_rec), any_ref = __any_sync(FULL, bad_ref);
+    const bool any_bad = __any_sync(FULL, bad_lane) || bad_sz;
     const bool de_ok = __all_sync(FULL, !has || src + L <= og || src >= op);
-    if (lane == 0) {
-      if (any_ref || any_rec || bad_sz)
-        report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
-      sts32(flg + w * 4, ((any_ref || any_rec || bad_sz) ? 1u : 0u) | (de_ok ? 0u : 6u));
+    const uint32_t myfl = (any_bad ? 1u : 0u) | (de_ok ? 0u : 2u);
+    if (lane == 0) sts32(flg + w * 4, myfl);
+    if (any_bad) {
+      const bool any_rec = __any_sync(FULL, act && !L && (r >> 16) != 0);
+      if (lane == 0) report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
     }
-    __syncthreads();
+    // fast path: the batch fits the zero-ahead distance, its literals have landed, and the ring holds the
+    // window, this batch and the next batch's zeroed range without touching unflushed output
+    const uint32_t landed = lf > 2 * kLzLUnit ? lf - 2 * kLzLUnit : 0u;
+    const bool room = OT <= kLzBatchMaxOut && a.window + 2 * kLzBatchMaxOut <= RING &&
+                      oB + OT + kLzBatchMaxOut - flushed <= RING;
     uint32_t fl = 0;
+    if (__syncthreads_or(myfl != 0)) {
 #pragma unroll
-    for (uint32_t ww = 0; ww < kBW; ++ww) fl |= lds32(flg + ww * 4);
+      for (uint32_t ww = 0; ww < kBW; ++ww) fl |= lds32(flg + ww * 4);
+    }
     if (fl & 1u) return;                                       // device error already reported
-    const bool batch_fast = !(fl & 2u) && OT <= kBatchMaxOut && LT + 32 <= kBatchLbuf && OT + a.window + 16 <= RING &&
-                            oB + OT - flushed <= RING;
-    if (batch_fast) {
-      // stage the batch's literal bytes [lB, lB + LT) (16-byte chunks) into the literal buffer
-      const uint8_t* la = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(lits + lB) & ~uintptr_t(15));
-      const uint32_t lofs = uint32_t((lits + lB) - la), nch = (lofs + LT + 15) / 16;
-      for (uint32_t c = threadIdx.x; c < nch; c += 32 * kBW) cp_async16(lbuf_s + 16 * c, la + 16 * c);
-      cp_commit();
-      // descriptors (batch-relative): start, literal end | own << 31, literal delta, match delta (own: literal
-      // buffer, else the distance); one start bit per non-empty sequence; and per row r >= 1 the number of
-      // sequences starting before it (written by the sequence holding byte 32r - 1)
-      const uint32_t y0 = op - oB, y1 = y0 + lit + L, ldl = lp - lB + lofs - y0;
-      const bool own = has && src >= op;
-      if ((ne >> lane) & 1u) {
-        const uint32_t jj = dbase + __popc(ne & lt);
-        sts128(desc_s + jj * 16, make_uint4(y0, (y0 + lit) | (own ? 0x80000000u : 0u), ldl, own ? ldl - dist : dist));
-        ats_or(rows_s + (y0 >> 5) * 8, 1u << (y0 & 31));
-        for (uint32_t rr = (y0 + 32) >> 5; rr <= (y1 >> 5) && rr * 32 < OT; ++rr) sts32(rows_s + rr * 8 + 4, jj + 1);
-      }
-      if (threadIdx.x == 0) sts32(rows_s + 4, 0u);
+    bool fast = !(fl & 2u) && room && lofs + lB + LT <= landed;
+    if (!fast && !(fl & 2u) && room && lofs + lB + LT <= lf) {
+      // the batch's literals are issued but maybe still in flight: wait for all of them (uniform, rare)
       cp_wait_n<0>();
       __syncthreads();
-      const uint32_t nrows = (OT + 31) / 32;
-      // a6 + a7: the batch's byte rows, kBW rows per step (row r by warp r % kBW), a CTA barrier per step
-      BatchView bv{ring, RM, desc_s, rows_s, lbuf_s, oB, oB};
-      for (uint32_t s0 = 0; s0 < nrows; s0 += kBW * kLzRPS) {
-        bv.sB = oB + s0 * 32;
-        uint32_t val[kLzRPS];
-#pragma unroll
-        for (uint32_t k = 0; k < kLzRPS; ++k) {
-          const uint32_t row = s0 + w + kBW * k, y = row * 32 + lane;
-          val[k] = 0;
-          if (y < OT) {
-            const uint2 bp = lds64(rows_s + row * 8);
-            const uint32_t j = bp.y + __popc(bp.x & le) - 1u;
-            const uint4 D = lds128(desc_s + j * 16);
-            // literal byte, own-literal match byte (both in the literal buffer) or match byte in the ring
-            const bool isl = y < (D.y & 0x7fffffffu), inbuf = isl || (D.y >> 31);
-            const uint32_t q = oB + y - D.w;
-            const uint32_t sa = inbuf ? lbuf_s + y + (isl ? D.z : D.w) : ring + (q & RM);
-            val[k] = (inbuf || q < bv.sB) ? lds8(sa) : chase_byte(bv, q);
-          }
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < kLzRPS; ++k) {
-          const uint32_t y = (s0 + w + kBW * k) * 32 + lane;
-          if (y < OT) sts8(ring + ((oB + y) & RM), val[k]);
-        }
-        __syncthreads();
-      }
+      fast = true;
+    }
+    if (fast) {
+      // a6: literal string of each sequence from the literal ring into the output ring
+      if (act && lit) or_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+      // a7 (DE, one round): named barrier w (64 threads) passes warp w-1's "done" to warp w; a warp that needs
+      // nothing from the batch copies first and consumes the barrier afterwards, so its own "done" still
+      // implies all earlier ones
+      const bool need = __any_sync(FULL, has && src < op && src + L > oB);
+      if (w > 0 && need) chain_sync(w);
+      if (has) or_copy(ring, RM, dst, ring, RM, src, L);
+      if (w > 0 && !need) chain_sync(w);
+      if (w + 1 < kBW) chain_arrive(w + 1);
+      // zero the next batch's range (beyond everything this batch writes or reads)
+      const uint32_t zt = (oB + OT + kLzBatchMaxOut + 15u) & ~15u;
+      for (uint32_t p = zf + 16 * threadIdx.x; p < zt; p += 16 * 32 * kBW) sts128(ring + (p & RM), make_uint4(0u, 0u, 0u, 0u));
+      zf = max(zf, zt);
       if (STATS) {
         const uint32_t any = __ballot_sync(FULL, has);
         uint32_t bytes = has ? L : 0u;
@@ -1345,14 +1371,6 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
           if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
         }
-      }
-      for (uint32_t row = threadIdx.x; row < nrows; row += 32 * kBW) sts32(rows_s + row * 8, 0u);
-      // flush completed 16-byte chunks (all warps), at least kFlushBytes at a time
-      const uint32_t q1 = (oB + OT) >> 4;
-      if (q1 * 16 >= flushed + kFlushBytes) {
-        for (uint32_t q = (flushed >> 4) + threadIdx.x; q < q1; q += 32 * kBW)
-          reinterpret_cast<uint4*>(out)[q] = lds128(ring + ((q * 16) & RM));
-        flushed = q1 * 16;
       }
     } else {
       // slow batch (too large for the buffers, or not DE): flush the ring, then warp 0 runs the groups of the
@@ -1364,7 +1382,7 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
         for (uint32_t ww = 0; ww < kBW; ++ww) {
           const uint32_t gg = B0 + ww, ii = gg * 32 + lane;
           if (gg >= ngroups) break;
-          if (STATS && lane == 0 && (lds32(flg + ww * 4) & 4u)) atomicAdd(stats_ptr(a) + 66, 1ull);
+          if (STATS && lane == 0 && (lds32(flg + ww * 4) & 2u)) atomicAdd(stats_ptr(a) + 66, 1ull);
           const bool act2 = ii < n_seq;
           const uint32_t r2 = act2 ? __ldg(recs + ii) : 0u;
           const uint32_t lit2 = r2 & 1023u, mc2 = (r2 >> 10) & 63u, dist2 = (r2 >> 16) + 1u;
@@ -1375,9 +1393,9 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           if (!resolve_group<GOMP_STRAT_MRR, STATS>(a, go, lane, act2 && L2, dst2, dst2 - dist2, L2, op2, b, gg * 32))
             break;
           __syncwarp();
-          const uint4 tu = lds128(tab + ww * 16);
-          og2 += tu.x;
-          lg2 += tu.y;
+          const uint32_t tu = lds32(tab + ww * 4);
+          og2 += tu >> 16;
+          lg2 += tu & 0xffffu;
         }
       }
       __syncthreads();
@@ -1385,11 +1403,20 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       const uint32_t keep = min(o_new, max(a.window, 16u) + 16u);
       for (uint32_t p = o_new - keep + threadIdx.x; p < o_new; p += 32 * kBW) sts8(ring + (p & RM), out[p]);
       flushed = o_new;
-      __syncthreads();
+      // restart the zero-ahead frontier at the new output end
+      const uint32_t z16 = (o_new + 15u) & ~15u;
+      if (threadIdx.x < z16 - o_new) sts8(ring + ((o_new + threadIdx.x) & RM), 0u);
+      zf = (o_new + kLzBatchMaxOut + 15u) & ~15u;
+      for (uint32_t p = z16 + 16 * threadIdx.x; p < zf; p += 16 * 32 * kBW) sts128(ring + (p & RM), make_uint4(0u, 0u, 0u, 0u));
+      // literal staging restarts at the next batch's literals (everything issued has landed)
+      cp_wait_n<0>();
+      lf = max(lf, (lofs + lB + LT) / kLzLUnit * kLzLUnit);
     }
+    lB_prev = lB;
     oB += OT;
     lB += LT;
   }
+  cp_wait_n<0>();
   __syncthreads();
   if (oB != ulen || lB != e.n_lit) {
     if (threadIdx.x == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
@@ -1467,7 +1494,7 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   a.n_sub_total = info->n_sub_total;
   a.nb_total = info->n_blocks;
   a.ring_bytes = 16384;
-  while (a.ring_bytes < info->window_size + 4096) a.ring_bytes <<= 1;
+  while (a.ring_bytes < info->window_size + 2 * kLzBatchMaxOut) a.ring_bytes <<= 1;
   const bool byte_mode = info->mode == GOMP_MODE_BYTE;
   if (!byte_mode && !lz77_only) {
     const uint64_t nb = std::max<uint32_t>(info->n_blocks, 1);
