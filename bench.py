@@ -33,6 +33,10 @@ CONFIGS = {
            "C1: 1 MiB English-like text, Gompresso/Byte, 64 KiB blocks, DE"),
     "C2": ("wiki", 256 << 20, 2, dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16),
            "C2: 256 MiB Wikipedia-shaped text, Gompresso/Bit, 256 KiB blocks, 16 sub-blocks/block, DE"),
+    "C2-g128": ("wiki", 256 << 20, 2, dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16,
+                                         de_group=128),
+                "256 MiB Wikipedia-shaped text, Gompresso/Bit, 256 KiB blocks, 16 sub-blocks/block, DE over "
+                "128-sequence groups (SURVEY 8(f) f3)"),
     "C2-byte": ("wiki", 256 << 20, 2, dict(mode="byte", de=True, block_size=262144),
                 "256 MiB Wikipedia-shaped text, Gompresso/Byte, 256 KiB blocks, DE"),
     "C2-S16": ("wiki", 256 << 20, 2, dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16),

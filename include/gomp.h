@@ -81,6 +81,9 @@ typedef struct {
   uint32_t min_staleness;        /* match_finder 1: replace a table entry only if older than this; default 1024 */
   uint32_t max_chain;            /* match_finder 0: candidates examined per position, 0 = unlimited */
   uint32_t n_threads;            /* host compressor threads, 0 = all hardware threads */
+  uint32_t de_group;             /* DE group: sequences per warpHWM update, a multiple of 32 up to
+                                    224; default 32 (the paper's warp group). 128 = one group per
+                                    4-warp LZ77 batch: no source of a batch lies inside it */
 } gomp_params;
 
 /* Host copy of the 64-byte file header (FORMAT.md §1). */
@@ -92,6 +95,7 @@ typedef struct {
   uint32_t n_sub_total;
   uint32_t max_block_tokens;
   uint32_t mode, de, block_size, window_size, min_match, max_match, cwl, version;
+  uint32_t de_group;   /* header byte 10 */
 } gomp_info;
 
 /* First device-detected error. status = gomp_status, block = data block index, detail = kernel-specific. */

@@ -28,16 +28,16 @@ class OracleError(Exception):
 class Params(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "mode", "de", "block_size", "window_size", "min_match", "max_match", "sub_block_seqs",
-        "sub_blocks_per_block", "cwl")]
+        "sub_blocks_per_block", "cwl", "de_group")]
 
 
 def params(mode="byte", de=True, block_size=262144, window_size=8192, min_match=4, max_match=64,
-           sub_block_seqs=16, sub_blocks_per_block=0, cwl=10):
+           sub_block_seqs=16, sub_blocks_per_block=0, cwl=10, de_group=32):
     """Defaults = the paper's setup: 256 KB blocks, 8 KB window, 64-byte lookahead,
     16-sequence sub-blocks, CWL 10; min_match 4 (reading R8)."""
     m = {"byte": 0, "bit": 1}[mode] if isinstance(mode, str) else int(mode)
     return Params(m, int(bool(de)), block_size, window_size, min_match, max_match, sub_block_seqs,
-                  sub_blocks_per_block, cwl)
+                  sub_blocks_per_block, cwl, de_group)
 
 
 def _lib():

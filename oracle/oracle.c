@@ -45,6 +45,7 @@ typedef struct {
   uint32_t sub_block_seqs;       /* S; 0 = use sub_blocks_per_block */
   uint32_t sub_blocks_per_block;
   uint32_t cwl;
+  uint32_t de_group;             /* sequences per DE group (warpHWM update period); 0 = 32 (the paper's warp) */
 } or_params;
 
 /* ------------------------------------------------------------------ little-endian helpers */
@@ -68,9 +69,12 @@ static void sv_push(seqvec *s, uint32_t lit, uint32_t L, uint32_t dist) {
  * prefix capped by max_match, by n-c (block end) and by c-s (no overlap, R2). With DE (Fig. alg:dedeflate),
  * a candidate is admissible iff s >= ls (inside the pending literal string) or s < warpHWM, in which case its
  * length is also capped by warpHWM - s (R4/R5). The longest admissible candidate wins, ties to the smallest
- * distance (R7). warpHWM <- c after every 32nd emitted sequence (line alg:deupdate).
+ * distance (R7). warpHWM <- c after every 32nd emitted sequence (line alg:deupdate), or after every
+ * de_group-th sequence for the wide DE groups of FORMAT.md §4 (P:82-85 gives the group size
+ * as the warp width, a Kepler synchronisation choice).
  */
 static void parse_block(const uint8_t *src, uint32_t n, const or_params *p, seqvec *out) {
+  const uint32_t G = p->de_group ? p->de_group : 32;
   uint32_t c = 0, ls = 0, nseq = 0, hwm = 0;
   while (c < n) {
     uint32_t best_len = 0, best_dist = 0;
@@ -90,13 +94,13 @@ static void parse_block(const uint8_t *src, uint32_t n, const or_params *p, seqv
     if (best_len >= p->min_match) {
       sv_push(out, c - ls, best_len, best_dist);
       c += best_len; ls = c; nseq++;
-      if (nseq % 32 == 0) hwm = c;
+      if (nseq % G == 0) hwm = c;
     } else {
       c++;
       if (c - ls == 1023) {                      /* R10: close the run at 1023 literals */
         sv_push(out, 1023, 0, 0);
         ls = c; nseq++;
-        if (nseq % 32 == 0) hwm = c;
+        if (nseq % G == 0) hwm = c;
       }
     }
   }
@@ -227,7 +231,8 @@ int or_compress(const uint8_t *src, uint64_t n, const or_params *p, uint8_t *dst
   if (!p || p->block_size < 16 || p->block_size % 16 || p->window_size < 1 || p->window_size > 32768 ||
       (p->min_match != 3 && p->min_match != 4) || p->max_match < p->min_match ||
       p->max_match > p->min_match + 62 || p->mode > 1 ||
-      (p->mode == 1 && (p->cwl < 9 || p->cwl > 15 || (p->sub_block_seqs == 0 && p->sub_blocks_per_block == 0))))
+      (p->mode == 1 && (p->cwl < 9 || p->cwl > 15 || (p->sub_block_seqs == 0 && p->sub_blocks_per_block == 0))) ||
+      p->de_group % 32 || p->de_group > 224)
     return OR_INVALID_ARG;
   uint32_t nb = (uint32_t)((n + p->block_size - 1) / p->block_size);
   seqvec *seqs = (seqvec *)calloc(nb ? nb : 1, sizeof(seqvec));
@@ -349,7 +354,7 @@ int or_compress(const uint8_t *src, uint64_t n, const or_params *p, uint8_t *dst
   memcpy(h, "GMPR", 4);
   h[4] = 1; h[5] = (uint8_t)p->mode; h[6] = (uint8_t)(p->de ? 1 : 0);
   h[7] = (uint8_t)p->min_match; h[8] = (uint8_t)p->max_match; h[9] = (uint8_t)(p->mode ? p->cwl : 0);
-  h[10] = 32; h[11] = 0;
+  h[10] = (uint8_t)(p->de_group ? p->de_group : 32); h[11] = 0;
   wr32(h + 12, p->block_size); wr32(h + 16, p->window_size); wr32(h + 20, nb);
   wr64(h + 24, n); wr64(h + 32, pos);
   wr32(h + 40, (uint32_t)n_sub_total); wr32(h + 44, p->mode ? max_tokens : 0);
@@ -362,7 +367,7 @@ int or_compress(const uint8_t *src, uint64_t n, const or_params *p, uint8_t *dst
 
 /* ------------------------------------------------------------------ reader */
 typedef struct {
-  uint32_t mode, de, min_match, max_match, cwl, block_size, window, nb, n_sub_total, max_tokens;
+  uint32_t mode, de, min_match, max_match, cwl, block_size, window, nb, n_sub_total, max_tokens, de_group;
   uint64_t total, file_len, payload_base;
 } or_hdr;
 
@@ -373,8 +378,9 @@ static int read_header(const uint8_t *f, uint64_t len, or_hdr *h) {
   h->mode = f[5]; h->de = f[6] & 1; h->min_match = f[7]; h->max_match = f[8]; h->cwl = f[9];
   h->block_size = rd32(f + 12); h->window = rd32(f + 16); h->nb = rd32(f + 20);
   h->total = rd64(f + 24); h->file_len = rd64(f + 32); h->n_sub_total = rd32(f + 40);
-  h->max_tokens = rd32(f + 44); h->payload_base = rd64(f + 48);
-  if (h->mode > 1 || (f[6] & ~1u) || f[10] != 32 || f[11] || rd32(f + 56) || rd32(f + 60)) return OR_HEADER_INCONSISTENT;
+  h->max_tokens = rd32(f + 44); h->payload_base = rd64(f + 48); h->de_group = f[10];
+  if (h->mode > 1 || (f[6] & ~1u) || f[10] == 0 || f[10] % 32 || f[11] || rd32(f + 56) || rd32(f + 60))
+    return OR_HEADER_INCONSISTENT;
   if (h->min_match != 3 && h->min_match != 4) return OR_HEADER_INCONSISTENT;
   if (h->max_match < h->min_match || h->max_match > h->min_match + 62) return OR_HEADER_INCONSISTENT;
   if (h->block_size < 16 || h->block_size % 16 || h->window < 1 || h->window > 32768) return OR_HEADER_INCONSISTENT;
@@ -708,7 +714,7 @@ int or_verify_de(const uint8_t *f, uint64_t len) {
     }
     uint32_t o = 0, H = 0;
     for (uint32_t i = 0; i < sv.n; i++) {
-      if (i % 32 == 0) H = o;
+      if (i % h.de_group == 0) H = o;
       seq_t q = sv.v[i];
       uint32_t ls = o, d = o + q.lit_len;
       if (q.L) {

@@ -42,14 +42,14 @@ class GompError(RuntimeError):
 class Params(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "struct_size", "mode", "de", "block_size", "window_size", "min_match", "max_match", "sub_block_seqs",
-        "sub_blocks_per_block", "cwl", "match_finder", "min_staleness", "max_chain", "n_threads")]
+        "sub_blocks_per_block", "cwl", "match_finder", "min_staleness", "max_chain", "n_threads", "de_group")]
 
 
 class Info(ctypes.Structure):
     _fields_ = [("uncompressed_len", ctypes.c_uint64), ("file_len", ctypes.c_uint64),
                 ("payload_base", ctypes.c_uint64), ("n_blocks", ctypes.c_uint32), ("n_sub_total", ctypes.c_uint32),
                 ("max_block_tokens", ctypes.c_uint32)] + [(n, ctypes.c_uint32) for n in (
-                    "mode", "de", "block_size", "window_size", "min_match", "max_match", "cwl", "version")]
+                    "mode", "de", "block_size", "window_size", "min_match", "max_match", "cwl", "version", "de_group")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -111,7 +111,7 @@ def _check(st, where):
 
 def params(mode="bit", de=True, block_size=262144, window_size=8192, min_match=4, max_match=64,
            sub_block_seqs=None, sub_blocks_per_block=0, cwl=10, match_finder=0, min_staleness=1024, max_chain=0,
-           n_threads=0):
+           n_threads=0, de_group=32):
     """gomp_params; defaults = the paper's setup. Passing sub_blocks_per_block (k) selects the
     "k sub-blocks per block" parametrisation (BASELINE config C2) unless sub_block_seqs is also given."""
     p = Params()
@@ -121,7 +121,7 @@ def params(mode="bit", de=True, block_size=262144, window_size=8192, min_match=4
     vals = dict(mode=MODES[mode] if isinstance(mode, str) else int(mode), de=int(bool(de)), block_size=block_size,
                 window_size=window_size, min_match=min_match, max_match=max_match, sub_block_seqs=sub_block_seqs,
                 sub_blocks_per_block=sub_blocks_per_block, cwl=cwl, match_finder=match_finder,
-                min_staleness=min_staleness, max_chain=max_chain, n_threads=n_threads)
+                min_staleness=min_staleness, max_chain=max_chain, n_threads=n_threads, de_group=de_group)
     for k, v in vals.items():
         setattr(p, k, int(v))
     return p

@@ -68,9 +68,10 @@ void parse_block(const uint8_t* src, uint32_t n, const gomp_params& p, std::vect
   s.head.assign(size_t(1) << hbits, -1);
   if (p.match_finder == 0) s.prev.resize(n > 0 ? n : 1);
   uint32_t c = 0, ls = 0, nseq = 0, hwm = 0, ins = 0;
+  const uint32_t G = p.de_group;
   auto emit = [&](uint32_t lit, uint32_t L, uint32_t d) {
     out.push_back({lit, L, d});
-    if (++nseq % kGroup == 0) hwm = c;  // warpHWM <- pos after every 32 sequences
+    if (++nseq % G == 0) hwm = c;  // warpHWM <- pos after every de_group (32) sequences
   };
   while (c < n) {
     // index every position < c that can start a min_match-byte match
@@ -284,6 +285,7 @@ bool params_ok(const gomp_params* p) {
   if (p->mode > 1 || p->block_size < 16 || p->block_size % 16 || p->window_size < 1 || p->window_size > 32768) return false;
   if ((p->min_match != 3 && p->min_match != 4) || p->max_match < p->min_match || p->max_match > p->min_match + 62) return false;
   if (p->match_finder > 1) return false;
+  if (p->de_group == 0 || p->de_group % kGroup || p->de_group > 224) return false;
   if (p->mode == GOMP_MODE_BIT) {
     if (p->cwl < 9 || p->cwl > 15) return false;
     if (p->sub_block_seqs == 0 && p->sub_blocks_per_block == 0) return false;
@@ -325,6 +327,7 @@ __attribute__((visibility("default"))) void gomp_params_default(gomp_params* p) 
   p->min_staleness = 1024;
   p->max_chain = 0;
   p->n_threads = 0;
+  p->de_group = kGroup;     // 32-sequence warp groups
 }
 
 __attribute__((visibility("default"))) size_t gomp_compress_bound(size_t src_len, const gomp_params* p) {
@@ -417,7 +420,7 @@ __attribute__((visibility("default"))) gomp_status gomp_compress(const uint8_t* 
   h[7] = uint8_t(p->min_match);
   h[8] = uint8_t(p->max_match);
   h[9] = uint8_t(p->mode == GOMP_MODE_BIT ? p->cwl : 0);
-  h[10] = kGroup;
+  h[10] = uint8_t(p->de_group);
   h[11] = 0;
   st32(h + 12, p->block_size);
   st32(h + 16, p->window_size);

@@ -50,7 +50,8 @@ inline gomp_status parse_header(const uint8_t* h, size_t len, gomp_info* o) {
   i.n_sub_total = ld32(h + 40);
   i.max_block_tokens = ld32(h + 44);
   i.payload_base = ld64(h + 48);
-  bool ok = i.mode <= 1 && (h[6] & ~1u) == 0 && h[10] == kGroup && h[11] == 0 && ld32(h + 56) == 0 &&
+  i.de_group = h[10];
+  bool ok = i.mode <= 1 && (h[6] & ~1u) == 0 && h[10] != 0 && h[10] % kGroup == 0 && h[11] == 0 && ld32(h + 56) == 0 &&
             ld32(h + 60) == 0;
   ok = ok && (i.min_match == 3 || i.min_match == 4) && i.max_match >= i.min_match &&
        i.max_match <= i.min_match + 62;

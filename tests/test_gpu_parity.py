@@ -63,6 +63,19 @@ def test_bit_parity(kind, n, de, sub):
     _check(c, x, ["auto", "mrr"] if de else ["auto", "sc"])
 
 
+@pytest.mark.parametrize("group", [64, 128, 224])
+@pytest.mark.parametrize("kind,n", [("wiki", 1_100_003), ("nested8", 300_000), ("matrix", 500_001)])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_wide_de_group_parity(group, kind, n, mode):
+    """Wide DE groups: the batch LZ77 kernel needs no wait inside a 128-sequence batch."""
+    x = _data(kind, n)
+    kw = dict(sub_blocks_per_block=16, sub_block_seqs=0) if mode == "bit" else {}
+    c = gomp.compress(x, mode=mode, de=True, block_size=65536, de_group=group, **kw)
+    _check(c, x, ["auto", "mrr"])
+    _, st = _gpu(c, "de", return_stats=True)
+    assert st["de_fallback_groups"] == 0
+
+
 @pytest.mark.parametrize("cfg", [
     dict(block_size=16), dict(block_size=4096, window_size=1), dict(block_size=1 << 20),
     dict(block_size=32768, min_match=3, max_match=65), dict(block_size=32768, min_match=3, max_match=3),

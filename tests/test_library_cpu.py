@@ -58,6 +58,21 @@ def test_compressor_matches_oracle_bytes(kind, n, mode, de):
     assert np.array_equal(c, ref)
 
 
+@pytest.mark.parametrize("group", [64, 128])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_compressor_wide_de_groups_match_oracle(group, mode):
+    x = datagen.wiki(200_000, seed=6)
+    kw = dict(mode=mode, de=True, block_size=65536, de_group=group)
+    if mode == "bit":
+        kw.update(sub_block_seqs=0, sub_blocks_per_block=16)
+    c = gomp.compress(x, **kw).numpy()
+    assert np.array_equal(c, oracle.compress(x, **kw))
+    assert gomp.get_info(c).de_group == group
+    for bad in (0, 16, 48, 256):
+        with pytest.raises(gomp.GompError):
+            gomp.compress(x[:1000], **dict(kw, de_group=bad))
+
+
 @pytest.mark.parametrize("threads", [1, 3, 8])
 def test_compressor_deterministic_across_threads(threads):
     x = datagen.wiki(400_000, seed=9)

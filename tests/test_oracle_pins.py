@@ -108,13 +108,13 @@ def _brute_best(x, c, ls, hwm, p):
 
 
 @pytest.mark.parametrize("seed", range(12))
-@pytest.mark.parametrize("de", [False, True])
-def test_parse_is_greedy_longest(seed, de):
+@pytest.mark.parametrize("de,group", [(False, 32), (True, 32), (True, 64), (True, 128)])
+def test_parse_is_greedy_longest(seed, de, group):
     rng = np.random.default_rng(seed)
-    n = int(rng.integers(40, 220))
+    n = int(rng.integers(40, 220)) if group == 32 else int(rng.integers(24 * group, 30 * group))
     x = bytes(rng.choice(np.frombuffer(b"abc", np.uint8), size=n, p=[0.6, 0.3, 0.1]))
     p = dict(window=int(rng.integers(4, 40)), max=int(rng.integers(4, 12)), de=de, mm=3)
-    seqs = oracle.parse_block(x, min_match=3, max_match=p["max"], window_size=p["window"], de=de)
+    seqs = oracle.parse_block(x, min_match=3, max_match=p["max"], window_size=p["window"], de=de, de_group=group)
     c = 0
     hwm = 0
     for i, (l, L, d) in enumerate(seqs):
@@ -126,9 +126,11 @@ def test_parse_is_greedy_longest(seed, de):
         if L:
             assert _brute_best(x, c, ls, hwm, p) == (L, d)
             c += L
-        if (i + 1) % 32 == 0:
+        if (i + 1) % group == 0:   # warpHWM <- pos after every de_group-th sequence
             hwm = c
     assert c == len(x)
+    if group > 32:
+        assert len(seqs) > 2 * group, "the input must span several DE groups"
     assert expand(seqs, _literals(x, seqs)) == x
 
 
@@ -351,3 +353,24 @@ def test_bit_corruption_detected():
             assert e.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF")
             caught += 1
     assert caught == 40
+
+
+@pytest.mark.parametrize("group", [64, 128, 224])
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_wide_de_groups(group, mode):
+    """Wide DE groups: the header carries de_group, verify_de checks the rule per de_group
+    sequences, every de_group file is also a valid 32-group DE file (a wider group's start lies at or before
+    the start of each of its 32-sequence groups), and the round trip holds."""
+    x = datagen.wiki(150_000, seed=9)
+    kw = dict(mode=mode, de=True, block_size=65536, de_group=group)
+    if mode == "bit":
+        kw.update(sub_block_seqs=0, sub_blocks_per_block=16)
+    f = oracle.compress(x, **kw)
+    assert f[10] == group
+    assert oracle.verify_de(f) == 1
+    g = f.copy()
+    g[10] = 32
+    assert oracle.verify_de(g) == 1
+    assert np.array_equal(oracle.decompress(f), np.frombuffer(x, np.uint8) if isinstance(x, bytes) else x)
+    f32 = oracle.compress(x, **dict(kw, de_group=32))
+    assert len(f) >= len(f32) * 0.95   # wider groups only restrict the parse further (ratio cost reported)
