@@ -684,7 +684,9 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
     serial = seq_tot != nseq || lit_tot != nl || !tail_ok;
     if (!serial) {
       // ---------------- pass 2: decode from the true start, write records and literals
-      uint32_t ri = seq_inc - seqs, li = lit_inc - lits_t, run2 = runin, bad = 0, maxr = 0;
+      uint32_t* recp = rec + (seq_inc - seqs);
+      uint8_t* litp = lit + (lit_inc - lits_t);
+      uint32_t run2 = runin, bad = 0, maxr = 0;
       bool saw_eob = false;
       uint32_t at2 = S0 + t_start;
       const uint32_t stop = S0 + e_pos;
@@ -693,23 +695,24 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
         const uint32_t n = sym_decode<LONG>(rd, at2, t, E, D, r0, d32);
         at2 += n;
         const uint32_t kind = sym_kind(E);
-        if (kind == K_LIT) {
-          lit[li++] = uint8_t(E >> 16);
-          ++run2;
-        } else if (kind == K_LEN) {
-          const uint32_t L = sym_len(E, r0);
-          rec[ri++] = seq_record(run2, L, sym_dist(D, d32), mm1);
-          bad |= ((D >> 13) & 1u) | (L - a.min_match > lrange ? 1u : 0u);
-          maxr = max(maxr, run2);
-          run2 = 0;
-        } else {
+        if (kind >= K_EOB) {               // end of block or invalid code: leaves the loop (rare)
           if (kind == K_EOB) {
             saw_eob = true;
-            if (run2 != 0 && ri < nseq) rec[ri++] = run2;
+            if (run2 != 0 && recp < rec + nseq) *recp++ = run2;
           } else {
             bad = 1;
           }
           break;
+        }
+        if (kind == K_LIT) {
+          *litp++ = uint8_t(E >> 16);
+          ++run2;
+        } else {
+          const uint32_t L = sym_len(E, r0);
+          *recp++ = seq_record(run2, L, sym_dist(D, d32), mm1);
+          bad |= ((D >> 13) & 1u) | (L - a.min_match > lrange ? 1u : 0u);
+          maxr = max(maxr, run2);
+          run2 = 0;
         }
       }
       maxr = max(maxr, run2);
