@@ -1,0 +1,236 @@
+#!/usr/bin/env python
+"""bench_configs.py — the BASELINE.json configurations beside the headline bench line.
+
+    python bench_configs.py [--only C1,C3,C4,C5] [--steps K] > profiles/r01_configs.jsonl
+
+One JSON line per measured point, same timing rules as bench.py (CUDA events on the launching stream, W >= 3
+untimed warm-up steps, the 126 MB L2 flushed by a 512 MiB write between timed steps, device-resident inputs),
+every point checked against its input byte for byte before it is timed. value = uncompressed bytes / mean step
+time (GB/s, 1e9); roofline_frac = (compressed + uncompressed bytes) / step time / HBM peak.
+
+  C1  1 MiB English-like text, Byte, 64 KiB blocks, DE: single-launch latency and steady state (CUDA graph of
+      32 back-to-back decompressions), the oracle beside it on 1 core.
+  C3  256 MiB nesting-depth-D data (D = 1..32), Byte and Bit, MRR on the non-DE file vs DE on the DE
+      file, with the MRR rounds histogram measured on the GPU (GOMP_FLAG_STATS run, untimed).
+  C4  16 GiB Wikipedia-shaped corpus on one B200 = the C2 file's blocks tiled 64x (blocks are
+      independent and the window is 8 KiB, so tiling keeps per-block statistics).
+  C5  MatrixMarket-shaped numeric text, Bit, DE: block size x sub-blocks-per-block sweep (256 MiB per point on
+      one GPU; BASELINE names 4 GiB on 8 GPUs, i.e. 512 MiB per GPU).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import datagen  # noqa: E402
+import paper_1606_00519_b200 as gomp  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+FLUSH = None
+
+
+def timed(fn, k, w):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    for _ in range(w):
+        FLUSH.fill_(1)
+        fn()
+    torch.cuda.synchronize()
+    for i in range(k):
+        FLUSH.fill_(i & 0xff)
+        ev[i][0].record()
+        fn()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def point(tag, c, x_check, steps, strategy="auto", extra=None, stats=False):
+    """Time device-resident decompression of file c (host uint8 tensor); x_check(out) -> bool."""
+    info = gomp.get_info(c)
+    U, C = info.uncompressed_len, info.file_len
+    d = c.to(DEV)
+    out = torch.empty(U, dtype=torch.uint8, device=DEV)
+    ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device=DEV)
+    gomp.decompress_into(info, d, out, ws, strategy)
+    e = gomp.read_error(ws)
+    ok = e.status == 0 and bool(x_check(out))
+    ms = timed(lambda: gomp.decompress_into(info, d, out, ws, strategy), steps, 3)
+    t = statistics.mean(ms)
+    P, _ = bench.peaks()
+    line = {"config": tag, "value": round(U / (t * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(t, 4),
+            "uncompressed_bytes": U, "compressed_bytes": C, "ratio": round(U / C, 4), "strategy": strategy,
+            "mode": "bit" if info.mode else "byte", "de_file": bool(info.de), "block_size": info.block_size,
+            "n_blocks": info.n_blocks, "n_sub_total": info.n_sub_total,
+            "roofline_frac": round((U + C) / (t * 1e-3) / 1e9 / P, 4), "peak_gbs": P, "steps": steps,
+            "parity": ok}
+    if info.mode == 1:
+        kd = statistics.mean(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="decode"), 5, 3))
+        kl = statistics.mean(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="lz77"), 5, 3))
+        line["kernels_ms"] = {"huff_" + gomp.huff_variant(info): round(kd, 4), "lz77": round(kl, 4)}
+    if stats:
+        gomp.decompress_into(info, d, out, ws, strategy, stats=True)
+        st = gomp.read_stats(ws)
+        groups = sum(st["rounds"])
+        line["rounds_hist"] = {str(r): n for r, n in enumerate(st["rounds"]) if n}
+        line["mean_rounds"] = round(sum(r * n for r, n in enumerate(st["rounds"])) / max(groups, 1), 3)
+        line["de_fallback_groups"] = st["de_fallback_groups"]
+    if extra:
+        line.update(extra)
+    print(json.dumps(line), flush=True)
+    del d, out, ws
+    torch.cuda.empty_cache()
+    return line
+
+
+def run_c1(steps):
+    import oracle
+    x = datagen.text(1 << 20, seed=1)
+    c = gomp.compress(x, mode="byte", de=True, block_size=65536)
+    info = gomp.get_info(c)
+    xd = torch.from_numpy(x).to(DEV)
+    line = point("C1", c, lambda o: torch.equal(o, xd), steps, extra={"workload": bench.CONFIGS["C1"][4]})
+    # single-launch latency (host enqueue + kernel, synchronised) and steady state through a CUDA graph
+    d = c.to(DEV)
+    out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device=DEV)
+    ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device=DEV)
+    lat = []
+    for i in range(23):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gomp.decompress_into(info, d, out, ws)
+        torch.cuda.synchronize()
+        if i >= 3:
+            lat.append((time.perf_counter() - t0) * 1e6)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        gomp.decompress_into(info, d, out, ws, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(32):
+            gomp.decompress_into(info, d, out, ws, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(out, xd))
+    ms = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b) / 32)
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 3.0:
+        oracle.decompress(c.numpy())
+        reps += 1
+    cpu = info.uncompressed_len * reps / (time.perf_counter() - t0) / 1e9
+    print(json.dumps({"config": "C1-latency", "single_launch_us_median": round(statistics.median(lat), 1),
+                      "graph_steady_state_us": round(1e3 * statistics.median(ms), 2),
+                      "graph_steady_state_gbs": round(info.uncompressed_len / (statistics.median(ms) * 1e-3) / 1e9, 3),
+                      "oracle_1core_gbs": round(cpu, 4), "parity": ok and line["parity"]}), flush=True)
+
+
+def run_c3(steps):
+    for D in (1, 2, 4, 8, 16, 32):
+        x = datagen.nested(256 << 20, D, seed=3)
+        xd = torch.from_numpy(x).to(DEV)
+        for mode in ("byte", "bit"):
+            kw = dict(mode=mode, block_size=262144)
+            if mode == "bit":
+                kw.update(sub_block_seqs=16)
+            for de, strat in ((False, "mrr"), (True, "de")):
+                c = gomp.compress(x, de=de, **kw)
+                point(f"C3-D{D}-{mode}-{strat}", c, lambda o: torch.equal(o, xd), steps, strategy=strat, stats=True,
+                      extra={"depth": D, "workload": f"256 MiB nesting-depth-{D} data, Gompresso/{mode.capitalize()}, "
+                                                     f"{'DE file, DE' if de else 'non-DE file, MRR'}"})
+        del xd
+        torch.cuda.empty_cache()
+
+
+def tile_file(c, times):
+    """A valid file whose blocks are the blocks of c repeated `times` times (c's last block must be full)."""
+    a = c.numpy()
+    info = gomp.get_info(a)
+    nb, ns, U = info.n_blocks, info.n_sub_total, info.uncompressed_len
+    assert U == nb * info.block_size, "tiling needs full blocks"
+    bt = a[64:64 + 32 * nb].copy().view(np.uint32).reshape(nb, 8)
+    st = a[64 + 32 * nb:64 + 32 * nb + 8 * ns]
+    pb, pend = info.payload_base, info.file_len - 16
+    pay = a[pb:pend]
+    base = -(-(64 + 32 * nb * times + 8 * ns * times) // 16) * 16
+    total = base + len(pay) * times + 16
+    f = np.zeros(total, dtype=np.uint8)
+    f[:64] = a[:64]
+    hv = f[:64].view(np.uint32)
+    hv[5] = nb * times
+    f[24:32] = np.frombuffer(np.uint64(U * times).tobytes(), np.uint8)
+    f[32:40] = np.frombuffer(np.uint64(total).tobytes(), np.uint8)
+    hv[10] = ns * times
+    f[48:56] = np.frombuffer(np.uint64(base).tobytes(), np.uint8)
+    bts = np.tile(bt, (times, 1))
+    off = bt[:, 0].astype(np.uint64) | (bt[:, 1].astype(np.uint64) << np.uint64(32))
+    for r in range(times):
+        o = off - np.uint64(pb) + np.uint64(base + r * len(pay))
+        bts[r * nb:(r + 1) * nb, 0] = (o & np.uint64(0xffffffff)).astype(np.uint32)
+        bts[r * nb:(r + 1) * nb, 1] = (o >> np.uint64(32)).astype(np.uint32)
+        bts[r * nb:(r + 1) * nb, 5] = bt[:, 5] + np.uint32(r * ns)
+    f[64:64 + 32 * nb * times] = bts.reshape(-1).view(np.uint8)
+    f[64 + 32 * nb * times:64 + 32 * nb * times + 8 * ns * times] = np.tile(st, times)
+    f[base:base + len(pay) * times] = np.tile(pay, times)
+    return torch.from_numpy(f)
+
+
+def run_c4(steps):
+    kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+    x = bench.gen(kind, n, seed)
+    c = tile_file(gomp.compress(x, **ckw), 64)
+    xd = torch.from_numpy(x).to(DEV)
+
+    def check(o):
+        return all(torch.equal(o[i * n:(i + 1) * n], xd) for i in range(64))
+
+    point("C4-1gpu", c, check, max(3, steps // 4),
+          extra={"workload": "C4: 16 GiB Wikipedia-shaped corpus (C2 blocks tiled 64x), Gompresso/Bit, 256 KiB "
+                             "blocks, 16 sub-blocks/block, DE, 1 B200 (the driver's scaling run covers 2/4/8)"})
+
+
+def run_c5(steps):
+    x = datagen.matrix(256 << 20, seed=5)
+    xd = torch.from_numpy(x).to(DEV)
+    for bs in (65536, 131072, 262144, 524288, 1 << 20):
+        for sub in (4, 8, 16, 32, 64, "S16"):
+            kw = dict(mode="bit", de=True, block_size=bs)
+            kw.update(dict(sub_block_seqs=16) if sub == "S16" else dict(sub_blocks_per_block=sub))
+            c = gomp.compress(x, **kw)
+            point(f"C5-bs{bs // 1024}k-{'S16' if sub == 'S16' else f'k{sub}'}", c, lambda o: torch.equal(o, xd),
+                  steps, extra={"workload": "256 MiB MatrixMarket-shaped numeric text, Gompresso/Bit, DE",
+                                "sub_blocks": sub})
+
+
+def main():
+    global FLUSH
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C1,C3,C4,C5")
+    ap.add_argument("--steps", type=int, default=10)
+    args = ap.parse_args()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench_configs.py needs a CUDA device (no CPU fallback)")
+    FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
+    for name in args.only.split(","):
+        {"C1": run_c1, "C3": run_c3, "C4": run_c4, "C5": run_c5}[name](args.steps)
+
+
+if __name__ == "__main__":
+    main()

@@ -201,10 +201,10 @@ def token_bytes(c):
 
 def huff_variant(info):
     """Which Bit decoder the launcher picks (mirrors decompress_range): "warp" when the mean sub-block holds at
-    least 4 * 32 * 96 bits, else "thread"."""
+    least 8192 bits (kWarpMinAvgBits), else "thread"."""
     if not info.n_sub_total:
         return "thread"
-    return "warp" if (info.file_len - info.payload_base) * 8 // info.n_sub_total >= 4 * 32 * 96 else "thread"
+    return "warp" if (info.file_len - info.payload_base) * 8 // info.n_sub_total >= 8192 else "thread"
 
 
 def decompress_into(info, src, dst, workspace, strategy="auto", stream=None, first_block=0, n_blocks=None,

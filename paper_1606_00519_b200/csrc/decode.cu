@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
 // extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
 constexpr uint32_t kRec = 64;
 constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below G*this use one lane (serial)
+constexpr uint32_t kWarpMinAvgBits = 8192;  // launcher: mean sub-block bits from which K1b is used
 constexpr uint32_t kHuffWarps = 16;         // warps per CTA (one data block; its groups share its sub-blocks)
 constexpr uint32_t kHuffG = 2;              // warps per sub-block group
 constexpr uint32_t kXsBytes = 1024;         // per-group exchange area (shared memory)
@@ -1506,7 +1507,9 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const bool LONGc = info->cwl > a.lut_bits;
     const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << a.lut_bits) * sizeof(uint32_t);
     const int force = strategy & (GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP);
-    const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= 4 * kSpecMinBits;
+    // measured crossover (matrix data, 64 KiB-512 KiB blocks x 4-128 sub-blocks, profiles/r01_ncu_summary.md):
+    // the speculative warp decoder wins from ~11 kbit sub-blocks up, the thread decoder below ~6 kbit
+    const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= kWarpMinAvgBits;
     const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
     if (use_warp) {
       // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of kHuffG warps per sub-block, speculative
