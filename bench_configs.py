@@ -16,6 +16,7 @@ time (GB/s, 1e9); roofline_frac = (compressed + uncompressed bytes) / step time 
       independent and the window is 8 KiB, so tiling keeps per-block statistics).
   C5  MatrixMarket-shaped numeric text, Bit, DE: block size x sub-blocks-per-block sweep (256 MiB per point on
       one GPU; BASELINE names 4 GiB on 8 GPUs, i.e. 512 MiB per GPU).
+  f2  the GPU compressor (gomp_compress_device) beside the host compressor, identical files required.
 """
 import argparse
 import json
@@ -219,6 +220,39 @@ def run_c5(steps):
                                 "sub_blocks": sub})
 
 
+def run_f2(steps):
+    """GPU compressor: C2-shaped and C3/C5 inputs compressed on the device (input and file
+    resident), wall time of the gomp_compress_device call (it synchronises: the file layout needs the block
+    sizes), beside the host compressor on all host threads; the files must be identical."""
+    import os as _os
+    for tag, kind, n, seed, kw in [
+            ("f2-C2", "wiki", 256 << 20, 2, dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16)),
+            ("f2-C2-byte", "wiki", 256 << 20, 2, dict(mode="byte", de=True, block_size=262144)),
+            ("f2-C5", "matrix", 256 << 20, 5, dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16)),
+            ("f2-C3-D8", "nested8", 256 << 20, 3, dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16))]:
+        x = bench.gen(kind, n, seed)
+        xd = torch.from_numpy(x).to(DEV)
+        g = gomp.compress_device(xd, **kw)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, steps // 3)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g = gomp.compress_device(xd, **kw)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        h = gomp.compress(x, **kw)
+        th = time.perf_counter() - t0
+        same = bool(np.array_equal(g.cpu().numpy(), h.numpy()))
+        print(json.dumps({"config": tag, "gpu_compress_gbs": round(n / statistics.median(ts) / 1e9, 3),
+                          "gpu_compress_ms": round(1e3 * statistics.median(ts), 2),
+                          "host_compress_gbs": round(n / th / 1e9, 3), "host_threads": _os.cpu_count(),
+                          "ratio": round(n / g.numel(), 4), "identical_to_host": same}), flush=True)
+        del xd, g
+        torch.cuda.empty_cache()
+
+
 def main():
     global FLUSH
     ap = argparse.ArgumentParser()
@@ -229,7 +263,7 @@ def main():
         raise SystemExit("bench_configs.py needs a CUDA device (no CPU fallback)")
     FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
     for name in args.only.split(","):
-        {"C1": run_c1, "C3": run_c3, "C4": run_c4, "C5": run_c5}[name](args.steps)
+        {"C1": run_c1, "C3": run_c3, "C4": run_c4, "C5": run_c5, "f2": run_f2}[name](args.steps)
 
 
 if __name__ == "__main__":

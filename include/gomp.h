@@ -136,6 +136,25 @@ gomp_status gomp_compress(const uint8_t* src, size_t src_len, uint8_t* dst, size
                           const gomp_params* p);
 
 /*
+ * GPU compressor ("each block is LZ77-compressed by a group of threads"): the same
+ * file as gomp_compress for the same input and parameters, byte for byte, computed on the device current on
+ * the calling thread: one warp per block runs the greedy longest-match parse with DE (hash chains in shared
+ * memory, 32 candidates compared per warp step), Byte payloads or Huffman coding (frequencies, canonical
+ * codes and bit packing on the device; the package-merge code lengths on the host, as gomp_compress).
+ *   d_src      DEVICE input, src_len bytes (any alignment)
+ *   d_dst      DEVICE output, 16-byte aligned, capacity dst_cap >= gomp_compress_bound(src_len, p)
+ *   dst_len    HOST, receives the file size
+ *   d_workspace DEVICE scratch, 16-byte aligned, >= gomp_compress_device_workspace_size(src_len, p, ...)
+ *   p          parameters as gomp_compress; match_finder must be 0 and max_chain 0 (exhaustive parse)
+ *   stream     cudaStream_t; the call synchronises it (the file layout needs the per-block sizes)
+ * Errors: INVALID_ARG, WORKSPACE_TOO_SMALL, DST_TOO_SMALL, CUDA.
+ */
+gomp_status gomp_compress_device_workspace_size(size_t src_len, const gomp_params* p, size_t* bytes);
+gomp_status gomp_compress_device(const uint8_t* d_src, size_t src_len, uint8_t* d_dst, size_t dst_cap,
+                                 size_t* dst_len, void* d_workspace, size_t ws_bytes, const gomp_params* p,
+                                 void* stream);
+
+/*
  * Parse and validate the 64-byte file header from a HOST copy hdr[0..hdr_len) (hdr_len >= 64) into *out.
  * Checks magic, version, field ranges and the header-level consistency rules of FORMAT.md §1.
  * Errors: TRUNCATED (hdr_len < 64), BAD_MAGIC, UNSUPPORTED_VERSION, HEADER_INCONSISTENT.

@@ -68,7 +68,7 @@ _lib = None
 EXPORTS = ["gomp_version", "gomp_status_string", "gomp_params_default", "gomp_compress_bound", "gomp_compress",
            "gomp_get_info", "gomp_validate_tables", "gomp_decompress_workspace_size", "gomp_decompress",
            "gomp_decompress_blocks", "gomp_decompress_host", "gomp_decompress_error", "gomp_decompress_stats",
-           "gomp_plan_shards"]
+           "gomp_plan_shards", "gomp_compress_device_workspace_size", "gomp_compress_device"]
 
 
 def lib():
@@ -94,6 +94,9 @@ def lib():
     L.gomp_decompress.argtypes = [ctypes.POINTER(Info), u8p, sz, u8p, sz, vp, sz, ctypes.c_int, vp]
     L.gomp_decompress_blocks.argtypes = [ctypes.POINTER(Info), u32, u32, u8p, sz, u8p, sz, vp, sz, ctypes.c_int, vp]
     L.gomp_decompress_host.argtypes = [ctypes.POINTER(Info), u8p, sz, u8p, sz, u8p, u8p, vp, sz, ctypes.c_int, vp]
+    L.gomp_compress_device_workspace_size.argtypes = [sz, ctypes.POINTER(Params), ctypes.POINTER(ctypes.c_size_t)]
+    L.gomp_compress_device.argtypes = [u8p, sz, u8p, sz, ctypes.POINTER(ctypes.c_size_t), vp, sz,
+                                       ctypes.POINTER(Params), vp]
     L.gomp_decompress_error.argtypes = [vp, vp, ctypes.POINTER(Error)]
     L.gomp_decompress_stats.argtypes = [vp, vp, ctypes.POINTER(Stats)]
     L.gomp_plan_shards.argtypes = [u8p, sz, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
@@ -149,6 +152,27 @@ def compress(x, p=None, **kw):
     _check(lib().gomp_compress(src.ctypes.data if len(src) else None, len(src), out.ctypes.data, cap, ctypes.byref(n),
                                ctypes.byref(p)), "gomp_compress")
     return torch.from_numpy(out[: n.value].copy())
+
+
+def compress_device(x, p=None, stream=None, **kw):
+    """gomp_compress_device: compress a CUDA uint8 tensor on the GPU; returns the file as a CUDA uint8 tensor
+    (identical to compress() of the same bytes and parameters)."""
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.uint8 and x.is_contiguous()):
+        raise ValueError("compress_device() takes a contiguous CUDA uint8 tensor (no CPU fallback)")
+    p = p or params(**kw)
+    cap = lib().gomp_compress_bound(x.numel(), ctypes.byref(p))
+    if cap == 0:
+        raise GompError(-1, where="gomp_compress_bound")
+    wsn = ctypes.c_size_t(0)
+    _check(lib().gomp_compress_device_workspace_size(x.numel(), ctypes.byref(p), ctypes.byref(wsn)),
+           "gomp_compress_device_workspace_size")
+    out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    ws = torch.empty(max(wsn.value, 16), dtype=torch.uint8, device=x.device)
+    n = ctypes.c_size_t(0)
+    _check(lib().gomp_compress_device(x.data_ptr() if x.numel() else None, x.numel(), out.data_ptr(), cap,
+                                      ctypes.byref(n), ws.data_ptr(), ws.numel(), ctypes.byref(p),
+                                      _stream_ptr(stream, x.device)), "gomp_compress_device")
+    return out[: n.value]
 
 
 def get_info(c):

@@ -304,6 +304,34 @@ uint64_t block_bound(const gomp_params* p) {
 }
 
 }  // namespace
+
+// internal interface for the GPU compressor (compress_gpu.cu): the same parameter checks, package-merge and
+// header layout as the host compressor, so both produce identical files
+bool host_params_ok(const gomp_params* p) { return params_ok(p); }
+uint64_t host_max_seqs(uint32_t bs, uint32_t mm) { return max_seqs(bs, mm); }
+void host_package_merge(const uint64_t* freq, int n, int maxlen, uint8_t* lens) { package_merge(freq, n, maxlen, lens); }
+void host_write_header(uint8_t* h, const gomp_params* p, uint32_t nb, uint64_t src_len, uint64_t file_len,
+                       uint64_t n_sub_total, uint64_t max_tok, uint64_t base) {
+  std::memcpy(h, "GMPR", 4);
+  h[4] = 1;
+  h[5] = uint8_t(p->mode);
+  h[6] = p->de ? 1 : 0;
+  h[7] = uint8_t(p->min_match);
+  h[8] = uint8_t(p->max_match);
+  h[9] = uint8_t(p->mode == GOMP_MODE_BIT ? p->cwl : 0);
+  h[10] = uint8_t(p->de_group);
+  h[11] = 0;
+  st32(h + 12, p->block_size);
+  st32(h + 16, p->window_size);
+  st32(h + 20, nb);
+  st64(h + 24, src_len);
+  st64(h + 32, file_len);
+  st32(h + 40, uint32_t(n_sub_total));
+  st32(h + 44, p->mode == GOMP_MODE_BIT ? uint32_t(max_tok) : 0);
+  st64(h + 48, base);
+  st32(h + 56, 0);
+  st32(h + 60, 0);
+}
 }  // namespace gomp
 
 using namespace gomp;
@@ -412,26 +440,7 @@ __attribute__((visibility("default"))) gomp_status gomp_compress(const uint8_t* 
   }
   std::memset(dst + pos, 0, kTrailerBytes);
   pos += kTrailerBytes;
-  uint8_t* h = dst;
-  std::memcpy(h, "GMPR", 4);
-  h[4] = 1;
-  h[5] = uint8_t(p->mode);
-  h[6] = p->de ? 1 : 0;
-  h[7] = uint8_t(p->min_match);
-  h[8] = uint8_t(p->max_match);
-  h[9] = uint8_t(p->mode == GOMP_MODE_BIT ? p->cwl : 0);
-  h[10] = uint8_t(p->de_group);
-  h[11] = 0;
-  st32(h + 12, p->block_size);
-  st32(h + 16, p->window_size);
-  st32(h + 20, nb);
-  st64(h + 24, src_len);
-  st64(h + 32, pos);
-  st32(h + 40, uint32_t(n_sub_total));
-  st32(h + 44, p->mode == GOMP_MODE_BIT ? uint32_t(max_tok) : 0);
-  st64(h + 48, base);
-  st32(h + 56, 0);
-  st32(h + 60, 0);
+  host_write_header(dst, p, nb, src_len, pos, n_sub_total, max_tok, base);
   *dst_len = size_t(pos);
   return GOMP_OK;
 }
