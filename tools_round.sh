@@ -8,3 +8,4 @@ timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_
 timeout 900 python bench.py --impl reference > gpurun_out/${tag}_bench_reference.json 2>&1; tail -c 600 gpurun_out/${tag}_bench_reference.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"huff|lz77" -s 6 -c 2 -o gpurun_out/${tag}_prof python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu.log 2>&1; tail -1 gpurun_out/${tag}_ncu.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_torchrun.json 2> gpurun_out/${tag}_torchrun.err; tail -c 300 gpurun_out/${tag}_torchrun.json
