@@ -41,7 +41,7 @@ struct Args {
   uint8_t* tokens;        // Bit: token buffer, block i of the range at tokens + i * tok_stride
   uint8_t* ws;            // workspace base (error word, stats)
   uint64_t total, file_len, payload_base, tok_stride;
-  uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, lut_bits, max_tok;
+  uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, ll_bits, d_bits, max_tok;
   uint32_t n_sub_total, nb_total, ring_bytes;
 };
 
@@ -94,7 +94,9 @@ __constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 
                                          6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 
 // LUT entries (32 bits). litlen E: bits 0-4 bits spanned (code + extra; 0 = not resolvable by the table: a
-// long code), 5-8 code length, 9-10 kind, 11-13 extra-bit count, 16-24 literal byte or length base.
+// long code), 5-8 code length, 9-10 kind, 11-13 extra-bit count, 16-24 literal byte or length base. A literal
+// entry with bit 14 set is a PAIR: the index bits hold two whole literal codes; bits 0-4 span both, 5-8 are the
+// first code's length, 16-23 the first byte, 24-31 the second (one lookup, one iteration for two symbols).
 // distance D: 0-4 bits spanned, 5-8 code length, 9-12 extra-bit count, 13 invalid, 16-31 distance base.
 enum : uint32_t { K_LIT = 0, K_LEN = 1, K_EOB = 2, K_BAD = 3 };
 constexpr uint32_t kBadLL = 1u | (1u << 5) | (K_BAD << 9);   // invalid litlen code: spans 1 bit
@@ -230,7 +232,7 @@ struct GlobalBits {
 };
 
 struct Luts {
-  uint32_t ll, d, mask;   // shared-window addresses of the two tables, index mask
+  uint32_t ll, d, mask_ll, mask_d;   // shared-window addresses of the two tables, index masks
   const HuffSmem* sm;     // canonical description (codes longer than the table index)
 };
 
@@ -242,14 +244,14 @@ __device__ __forceinline__ uint32_t sym_decode(const RD& rd, uint32_t at, const 
                                                uint32_t& r0, uint32_t& d32) {
   uint32_t r1;
   rd.window(at, r0, r1);
-  E = ldsw(t.ll + ((r0 & t.mask) << 2));
+  E = ldsw(t.ll + ((r0 & t.mask_ll) << 2));
   if (LONG && (E & 31u) == 0) {                                  // code longer than the table index
     const int sl = canon_slow(r0, t.sm->tab[0], t.sm->sorted_ll);
     E = sl < 0 ? kBadLL : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
   }
   const uint32_t t1 = E & 31u;
   d32 = __funnelshift_r(r0, r1, t1);
-  D = ldsw(t.d + ((d32 & t.mask) << 2));
+  D = ldsw(t.d + ((d32 & t.mask_d) << 2));
   const bool isl = ((E >> 9) & 3u) == K_LEN;
   if (LONG && isl && (D & 31u) == 0) {
     const int sl = canon_slow(d32, t.sm->tab[1], t.sm->sorted_d);
@@ -258,6 +260,7 @@ __device__ __forceinline__ uint32_t sym_decode(const RD& rd, uint32_t at, const 
   return t1 + (isl ? (D & 31u) : 0u);
 }
 __device__ __forceinline__ uint32_t sym_kind(uint32_t E) { return (E >> 9) & 3u; }
+__device__ __forceinline__ uint32_t sym_pair(uint32_t E) { return (E >> 14) & 1u; }   // literal pair entry
 __device__ __forceinline__ uint32_t sym_len(uint32_t E, uint32_t r0) {      // match length (K_LEN)
   return (E >> 16) + ((r0 >> ((E >> 5) & 15u)) & ((1u << ((E >> 11) & 7u)) - 1u));
 }
@@ -270,7 +273,8 @@ __device__ __forceinline__ uint32_t sym_dist(uint32_t D, uint32_t d32) {
 // memory. Unresolved entries: 0 (LONG: canonical walk) or K_BAD. Returns false (uniformly) on a bad tree.
 template <bool LONG>
 __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, const uint8_t* pl, const Args& a) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lut_n = 1u << a.lut_bits;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t ll_n = 1u << a.ll_bits, d_n = 1u << a.d_bits;
   if (tid == 0) { sm.bad = 0; sm.next = 0; sm.carry_bits = 0; sm.carry_lits = 0; }
   if (tid < 16) {
     sm.tab[0].count[tid] = 0; sm.tab[0].running[tid] = 0;
@@ -327,19 +331,33 @@ __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, co
   }
   __syncthreads();
   if (sm.bad) return false;
-  const uint32_t LB = a.lut_bits;
-  for (uint32_t i = tid; i < 2 * lut_n; i += blockDim.x) {
-    const int t = i >= lut_n;
-    const uint32_t idx = i - (t ? lut_n : 0u);
-    const uint32_t v = __brev(idx) >> (32 - LB);      // code bits, first stream bit most significant
+  // canonical decode of the code at the head of `bits` (nb valid index bits, first stream bit = bit 0) with
+  // table t: symbol | length << 16, or 0xffffffff when no code of length <= nb matches
+  auto canon = [&](int t, uint32_t bits, uint32_t nb) -> uint32_t {
+    const uint32_t v = nb ? __brev(bits) >> (32 - nb) : 0u;   // code bits, first stream bit most significant
     const CanonTab& T = sm.tab[t];
+    for (uint32_t l = 1; l <= nb; ++l) {
+      const uint32_t code = v >> (nb - l);
+      if (code - T.first[l] < T.count[l])
+        return uint32_t(t ? sm.sorted_d[T.index[l] + code - T.first[l]] : sm.sorted_ll[T.index[l] + code - T.first[l]]) |
+               (l << 16);
+    }
+    return 0xffffffffu;
+  };
+  for (uint32_t i = tid; i < ll_n + d_n; i += blockDim.x) {
+    const int t = i >= ll_n;
+    const uint32_t idx = i - (t ? ll_n : 0u);
+    const uint32_t LB = t ? a.d_bits : a.ll_bits;
+    const uint32_t c1 = canon(t, idx, LB);
     uint32_t ent = LONG ? 0u : (t ? kBadD : kBadLL);  // unresolved: long code (LONG) or invalid
-    for (uint32_t l = 1; l <= LB; ++l) {
-      const uint32_t code = v >> (LB - l);
-      if (code - T.first[l] < T.count[l]) {
-        const uint32_t sym = t ? sm.sorted_d[T.index[l] + code - T.first[l]] : sm.sorted_ll[T.index[l] + code - T.first[l]];
-        ent = t ? d_entry(sym, l) : ll_entry(sym, l);
-        break;
+    if (c1 != 0xffffffffu) {
+      const uint32_t sym = c1 & 0xffffu, l1 = c1 >> 16;
+      ent = t ? d_entry(sym, l1) : ll_entry(sym, l1);
+      if (!t && sym < 256 && l1 < LB) {
+        // literal pair: the remaining LB - l1 index bits may hold a whole second literal code
+        const uint32_t c2 = canon(0, idx >> l1, LB - l1);
+        if (c2 != 0xffffffffu && (c2 & 0xffffu) < 256)
+          ent = (l1 + (c2 >> 16)) | (l1 << 5) | (K_LIT << 9) | (1u << 14) | (sym << 16) | ((c2 & 255u) << 24);
       }
     }
     (t ? lut_d : lut_ll)[idx] = ent;
@@ -372,6 +390,16 @@ __device__ uint32_t decode_sub_serial(const RD& rd, const Luts& t, const Args& a
     at += sym_decode<LONG>(rd, at, t, E, D, r0, d32);
     kind = sym_kind(E);
     const bool isl = kind == K_LEN, islit = kind == K_LIT;
+    if (islit && sym_pair(E)) {
+      if (run + 1 == kMaxLitRun) {
+        at -= (E & 31u) - ((E >> 5) & 15u);   // the first literal closes a run (R10): take it alone
+      } else {
+        if (lw < nl) lit[lw] = uint8_t(E >> 16);
+        ++lw;
+        ++run;
+        E = (E & ~0x00ff0000u) | ((E >> 8) & 0x00ff0000u);   // the second literal goes through the step below
+      }
+    }
     if (islit && lw < nl) lit[lw] = uint8_t(E >> 16);
     lw += islit ? 1u : 0u;
     run += islit ? 1u : 0u;
@@ -416,9 +444,9 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
-  const uint32_t lut_n = 1u << a.lut_bits;
-  uint32_t* lut_d = lut_ll + lut_n;
-  const uint32_t stage_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n));
+  const uint32_t ll_n = 1u << a.ll_bits, d_n = 1u << a.d_bits;
+  uint32_t* lut_d = lut_ll + ll_n;
+  const uint32_t stage_s = uint32_t(__cvta_generic_to_shared(lut_d + d_n));
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
@@ -432,7 +460,7 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
     return;
   }
   const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
-  const Luts t{lut_ll_s, lut_ll_s + lut_n * 4, lut_n - 1, &sm};
+  const Luts t{lut_ll_s, lut_ll_s + ll_n * 4, ll_n - 1, d_n - 1, &sm};
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint8_t* subt = a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total;
   uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
@@ -508,6 +536,8 @@ constexpr uint32_t kHuffG = 2;              // warps per sub-block group
 constexpr uint32_t kXsBytes = 1024;         // per-group exchange area (shared memory)
 constexpr uint32_t kStageMax = 48 * 1024;   // largest per-group bit stage (bytes)
 constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per CTA
+constexpr size_t kSmemPerSm = 228 * 1024;   // shared memory per SM (B200)
+constexpr size_t kSmemReservedPerCta = 1024;
 // exchange area layout (bytes): [0, 8V) exit records; 768 sub-block index; 784.. per-warp aggregates
 constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912;
 static_assert(8 * 32 * kHuffG <= kXsK && kHuffWarps % kHuffG == 0, "exchange area layout");
@@ -545,33 +575,39 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
     const uint32_t sp = S0 + vl * c;
     const uint32_t lim = S0 + min((vl + 1) * c, bsz);
     const uint32_t endb = S0 + bsz;
-    uint32_t at = sp, cnt = 0, lits = 0, run = 0, lm0 = 0, lm1 = 0;   // lm: literal iterations of 1a (bit it)
-    auto step1 = [&](uint32_t& islit) {
+    // iterations decode one symbol, or two literals (pair entry): liters counts literal iterations, lits
+    // literal bytes; lm/pm: literal / pair iterations among the first kRec (bit it)
+    uint32_t at = sp, cnt = 0, liters = 0, lits = 0, run = 0, lm0 = 0, lm1 = 0, pm0 = 0, pm1 = 0;
+    auto step1 = [&](uint32_t& islit, uint32_t& pair) {
       uint32_t E, D, r0, d32;
       const uint32_t n = sym_decode<LONG>(rd, at, t, E, D, r0, d32);
       const uint32_t kind = sym_kind(E);
       islit = kind == K_LIT ? 1u : 0u;
+      pair = sym_pair(E);
       cnt += 1;
-      lits += islit;
-      run = kind == K_LEN ? 0u : run + islit;
+      liters += islit;
+      lits += islit + pair;
+      run = kind == K_LEN ? 0u : run + islit + pair;
       return n;
     };
     // 1a: the first kRec iterations, recording the bits of each (boundary it+1 = boundary it + that)
 #pragma unroll 4
     for (uint32_t it = 0; it < 32; ++it) {
-      uint32_t n = 0, islit = 0;
-      if (at < endb) n = step1(islit);         // never decode past the end of the sub-block
+      uint32_t n = 0, islit = 0, pair = 0;
+      if (at < endb) n = step1(islit, pair);   // never decode past the end of the sub-block
       sts8(recs_s + it * V + vl, n);
       at += n;
       lm0 |= islit << it;
+      pm0 |= pair << it;
     }
 #pragma unroll 4
     for (uint32_t it = 32; it < kRec; ++it) {
-      uint32_t n = 0, islit = 0;
-      if (at < endb) n = step1(islit);
+      uint32_t n = 0, islit = 0, pair = 0;
+      if (at < endb) n = step1(islit, pair);
       sts8(recs_s + it * V + vl, n);
       at += n;
       lm1 |= islit << (it - 32);
+      pm1 |= pair << (it - 32);
     }
     gsync<G>(bar);
     // 1b: continue; past the chunk end, stop at the first boundary that a later lane also recorded: from there
@@ -593,8 +629,8 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
         }
         if (q < V && bq == rel) { exit_vl = q; exit_idx = ptr; break; }
       }
-      uint32_t islit;
-      at += step1(islit);
+      uint32_t islit, pair;
+      at += step1(islit, pair);
     }
     // ---------------- the true path: lane 0 starts at the sub-block start (its boundary 0) and hands over to
     // the lane it exited into, at that lane's recorded boundary; lanes it jumped over own nothing
@@ -629,14 +665,15 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       // statistics of the true segment = totals at the exit minus the counts before the merge boundary (all
       // `merged` iterations before it were decoded: the boundary lies before the sub-block end)
       const uint32_t m0 = min(merged, 32u), m1 = merged - m0;
-      const uint32_t lits0 = __popc(lm0 & (m0 == 32 ? FULL : (1u << m0) - 1u)) +
-                             __popc(lm1 & (m1 == 32 ? FULL : (1u << m1) - 1u));
-      const uint32_t nonlit0 = merged - lits0;
+      const uint32_t k0 = m0 == 32 ? FULL : (1u << m0) - 1u, k1 = m1 == 32 ? FULL : (1u << m1) - 1u;
+      const uint32_t liters0 = __popc(lm0 & k0) + __popc(lm1 & k1);
+      const uint32_t lits0 = liters0 + __popc(pm0 & k0) + __popc(pm1 & k1);
+      const uint32_t nonlit0 = merged - liters0;
       t_start = mpos;
       e_pos = e_rel;
       lits_t = lits - lits0;
       // non-literal symbols of the segment = length codes (+ the block's EOB at the very end of the tail lane)
-      nlen_t = (cnt - lits) - nonlit0 - ((last && is_tail) ? 1u : 0u);
+      nlen_t = (cnt - liters) - nonlit0 - ((last && is_tail) ? 1u : 0u);
       has_t = nlen_t != 0;
       trail_t = has_t ? run : lits_t;
     }
@@ -706,8 +743,11 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
           break;
         }
         if (kind == K_LIT) {
-          *litp++ = uint8_t(E >> 16);
-          ++run2;
+          const uint32_t pair = sym_pair(E);
+          *litp = uint8_t(E >> 16);
+          if (pair) litp[1] = uint8_t(E >> 24);
+          litp += 1 + pair;
+          run2 += 1 + pair;
         } else {
           const uint32_t L = sym_len(E, r0);
           *recp++ = seq_record(run2, L, sym_dist(D, d32), mm1);
@@ -751,11 +791,11 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
-  const uint32_t lut_n = 1u << a.lut_bits;
-  uint32_t* lut_d = lut_ll + lut_n;
+  const uint32_t ll_n = 1u << a.ll_bits, d_n = 1u << a.d_bits;
+  uint32_t* lut_d = lut_ll + ll_n;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t grp = warp / G, vl = tid % V, bar = 1 + grp;
-  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + lut_n)) + grp * group_slot_bytes(G, stage_cap);
+  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + d_n)) + grp * group_slot_bytes(G, stage_cap);
   const uint32_t recs_s = slot_s, xs_s = slot_s + V * kRec, stage_s = xs_s + kXsBytes;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
@@ -769,7 +809,7 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
     return;
   }
   const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
-  const Luts t{lut_ll_s, lut_ll_s + lut_n * 4, lut_n - 1, &sm};
+  const Luts t{lut_ll_s, lut_ll_s + ll_n * 4, ll_n - 1, d_n - 1, &sm};
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint32_t* subt = reinterpret_cast<const uint32_t*>(a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total) +
                          2ull * e.sub_first;
@@ -1493,7 +1533,8 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   a.min_match = info->min_match;
   a.max_match = info->max_match;
   a.cwl = info->cwl;
-  a.lut_bits = std::min<uint32_t>(info->cwl, kMaxLutBits);
+  a.ll_bits = kMaxLutBits;                              // literal/length table: 11 index bits (literal pairs)
+  a.d_bits = std::min<uint32_t>(info->cwl, kMaxLutBits);
   a.max_tok = info->max_block_tokens;
   a.n_sub_total = info->n_sub_total;
   a.nb_total = info->n_blocks;
@@ -1504,8 +1545,9 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const uint64_t nb = std::max<uint32_t>(info->n_blocks, 1);
     const uint64_t avg_sub = (uint64_t(info->n_sub_total) + nb - 1) / nb;
     const uint64_t avg_bits = info->n_sub_total ? (info->file_len - info->payload_base) * 8 / info->n_sub_total : 0;
-    const bool LONGc = info->cwl > a.lut_bits;
-    const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) + 2 * (size_t(1) << a.lut_bits) * sizeof(uint32_t);
+    const bool LONGc = info->cwl > kMaxLutBits;
+    const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) +
+                        ((size_t(1) << a.ll_bits) + (size_t(1) << a.d_bits)) * sizeof(uint32_t);
     const int force = strategy & (GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP);
     // measured crossover (matrix data, 64 KiB-512 KiB blocks x 4-128 sub-blocks, profiles/r01_ncu_summary.md):
     // the speculative warp decoder wins from ~11 kbit sub-blocks up, the thread decoder below ~6 kbit
@@ -1515,7 +1557,12 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of kHuffG warps per sub-block, speculative
       // decode; per group a bit stage of 1.3x the mean sub-block (+ slack); up to kHuffWarps/kHuffG groups per
       // CTA, as many as the sub-blocks of a block and the shared memory allow
-      const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * 13 / 10 + 96)));
+      // bit stage per group: 1.3x the mean sub-block (+ slack), but no more than lets two 16-warp CTAs share an SM
+      // (a sub-block larger than the stage reads its bits from L1/L2 instead)
+      const uint64_t two_per_sm = ((kSmemPerSm / 2 - kSmemReservedPerCta - tabs) / (kHuffWarps / kHuffG) -
+                                   32 * kHuffG * kRec - kXsBytes) & ~uint64_t(15);
+      const uint32_t cap = uint32_t(std::min<uint64_t>({kStageMax, align16(avg_bytes * 13 / 10 + 96),
+                                                        std::max<uint64_t>(two_per_sm, align16(avg_bytes + 96))}));
       const size_t slot = group_slot_bytes(kHuffG, cap);
       const uint64_t fit = (kSmemMax - tabs) / slot;
       const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / kHuffG, fit, avg_sub})));
