@@ -27,8 +27,7 @@ namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t kPipeStreams = 4;     // compute streams of the pipelined host path
-constexpr uint32_t kPipeMaxChunks = 8;   // chunks of the pipelined host path
-constexpr uint32_t kPipeMinBlocks = 64;  // fewest blocks per chunk
+constexpr uint32_t kPipeMaxChunks = 12;  // chunks of the pipelined host path (sizes double: small first chunks)
 constexpr int kLz77Warps = 2;        // warps (= data blocks) per CTA of the LZ77 kernel
 constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
 
@@ -1676,7 +1675,6 @@ GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_
   // chunking: payloads must be laid out in block order (our compressor does); otherwise one up-front copy
   const uint64_t tab_end = kHeaderBytes + uint64_t(kBlockEntryBytes) * nb;
   if (tab_end > flen) return GOMP_ERR_TRUNCATED;
-  uint32_t K = std::min<uint32_t>(kPipeMaxChunks, std::max<uint32_t>(1, (nb + kPipeMinBlocks - 1) / kPipeMinBlocks));
   std::vector<uint64_t> pend(nb);   // end of block b's payload (+ look-ahead), clamped to the file
   bool ordered = true;
   uint64_t prev = 0;
@@ -1687,7 +1685,20 @@ GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_
     prev = off;
     pend[b] = std::min<uint64_t>(flen, off + len + 64);
   }
-  if (!ordered) K = 1;
+  // chunk boundaries: sizes double from ~nb/128 blocks, so the first output is ready for the device->host copy
+  // after a short decode and the copy engine (the bottleneck of this path) starts early; one chunk if the
+  // payloads are not in block order
+  std::vector<uint32_t> cb{0};
+  {
+    uint32_t sz = std::max<uint32_t>(1, nb / 128);
+    while (ordered && cb.back() < nb && cb.size() < kPipeMaxChunks) {
+      cb.push_back(std::min<uint32_t>(nb, cb.back() + sz));
+      sz *= 2;
+    }
+    if (cb.back() < nb || cb.size() == 1) cb.push_back(nb);
+    if (!ordered) cb = {0, nb};
+  }
+  const uint32_t K = uint32_t(cb.size() - 1);
   Pipe p;
   if (!p.ok) return GOMP_ERR_CUDA;
   if (cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
@@ -1698,7 +1709,7 @@ GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_
   if (!ok) return GOMP_ERR_CUDA;
   uint64_t copied = 0;   // bytes [0, copied) of the file are enqueued host->device
   for (uint32_t i = 0; i < K; ++i) {
-    const uint32_t b0 = uint32_t(uint64_t(nb) * i / K), b1 = uint32_t(uint64_t(nb) * (i + 1) / K);
+    const uint32_t b0 = cb[i], b1 = cb[i + 1];
     const uint64_t hi = (i + 1 == K || !ordered) ? flen : std::max<uint64_t>(pend[b1 - 1], info->payload_base);
     if (hi > copied) {
       if (cudaMemcpyAsync(d_src_buf + copied, h_src + copied, hi - copied, cudaMemcpyHostToDevice, p.h2d) != cudaSuccess)
