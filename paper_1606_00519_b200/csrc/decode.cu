@@ -1,15 +1,17 @@
 // decode.cu — sm_100a kernels of the Gompresso decompression hot path and their C-ABI launchers.
 //
-//   huff_thread_kernel / huff_warp_kernel  Gompresso/Bit, one CTA per data block:
-//       a1 block-table entry checks; a2 CTA-wide exclusive scans of the sub-block bit sizes and literal counts
-//       (P:48-50); a3 canonical code lengths -> two 2^LB-entry lookup tables in shared memory
-//       (P:73-77); a4 one thread per sub-block decodes its bitstream with one table lookup per
-//       symbol into Byte-format records and literals in the workspace token buffer.
-//   lz77_kernel<STRAT>  one warp per data block, one sequence per lane: a5 read 32
-//       records + one packed warp exclusive scan giving both prefix sums; a6 literal
-//       copy; a7 back-references by Dependency Elimination (one round), Multi-Round Resolution
-//       (Fig. alg:mrr, HWM reading R1) or Sequential Copying. For Gompresso/Byte the
-//       same kernel reads the records straight from the file (a8, single pass).
+//   huff_thread_kernel (K1a) / huff_warp_kernel (K1b)  Gompresso/Bit, one CTA per data block:
+//       a1 block-table entry checks; a2 exclusive scans of the sub-block bit sizes and literal counts
+//       (P:48-50); a3 canonical code lengths -> two lookup tables in shared memory (P:73-77,
+//       P:656-659; literal-pair entries); a4 sub-block decode, one table lookup per symbol, into Byte-format
+//       records and literals in the workspace token buffer: K1a one thread per sub-block (the
+//       paper's scheme), K1b 64 lanes per sub-block with self-synchronising speculative starts.
+//   lz77_batch_kernel (K2b)  the DE strategy: 4 warps per data block take 4 consecutive 32-sequence groups, one
+//       sequence per lane: a5 record + one packed warp exclusive scan giving both prefix sums
+//       (P:105-112); a6 literal copy; a7 back-references in one round (Dependency Elimination,
+//       P:295-329). For Gompresso/Byte the records come straight from the file (a8, single pass).
+//   lz77_kernel<STRAT> (K2)  one warp per data block: Multi-Round Resolution (Fig. alg:mrr,
+//       P:174-253, HWM reading R1) or Sequential Copying for files without the DE property.
 //   a9 completion: first-error-wins error word and optional MRR statistics in the workspace.
 #include <cuda_runtime.h>
 
@@ -866,11 +868,10 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
 constexpr uint32_t kLitRing = 2048;
 constexpr uint32_t kLitUnit = 512;    // 32 lanes x 16 B per cp.async instruction
 constexpr uint32_t kLitAhead = 1024;  // prefetch distance in literal bytes
-constexpr uint32_t kPrmBytes = 32 * 16;  // the group's 32 sequence descriptors (DE pass)
 constexpr uint32_t kFlushBytes = 2048;   // ring -> HBM flush granularity
 
-// per-warp shared layout: [ring RING][literal ring 2 KiB][descriptors 512 B][row-start bitmap RING/8 B]
-__host__ __device__ constexpr uint32_t lz_warp_bytes(uint32_t ring) { return ring + kLitRing + kPrmBytes + ring / 8; }
+// per-warp shared layout: [output ring RING][literal ring 2 KiB]
+__host__ __device__ constexpr uint32_t lz_warp_bytes(uint32_t ring) { return ring + kLitRing; }
 
 // byte-granular copy without overlap (dist >= L, reading R2), global memory (slow path)
 __device__ __forceinline__ void copy_nolap(uint8_t* d, const uint8_t* s, uint32_t n) {
@@ -968,81 +969,6 @@ __device__ __forceinline__ bool resolve_group(const Args& a, const Out& o, uint3
   return true;
 }
 
-// DE group as word rows (a6 + a7 fused). Group-relative positions x in [0, T) (T = group output bytes).
-// Sequence i covers [opr_i, opr_{i+1}): literal part [opr_i, dst_i) whose byte x is lring[x + ld_i], match part
-// [dst_i, opr_{i+1}) whose byte x is (own_i ? lring : ring)[x + md_i] (own_i: source inside its own literal,
-// reading R4). Under the DE rule no source lies in this group's output, so every output word is a function of
-// final on-chip data: the group is written as rows of 32 aligned 32-bit words (lane t -> word t of the row).
-// The owner of a word's first byte comes from a bitmap of sequence starts (one RED.OR per lane) and popcounts;
-// a word touches at most two sequences, i.e. at most four segments (literal/match of the owner and of its
-// successor); each present segment contributes one funnel-shifted source word under a byte mask. Bytes of the
-// first word that precede the group are kept from the ring (final); bytes past the group in the last word are
-// rewritten by the next group. No inter-lane ordering, no divergence beyond predication.
-__device__ __forceinline__ uint32_t ring_word_at(uint32_t base, uint32_t mask, uint32_t p) {
-  const uint32_t i = p & ~3u;
-  return __funnelshift_r(lds32(base + (i & mask)), lds32(base + ((i + 4) & mask)), (p & 3u) * 8u);
-}
-__device__ __forceinline__ uint32_t byte_mask(int32_t a, int32_t b) {   // bytes [a, b) of a word, 0 <= a < b <= 4
-  return (0xffffffffu >> (32 - 8 * (b - a))) << (8 * a);
-}
-__device__ __forceinline__ void de_group_words(uint32_t ring, uint32_t RM, uint32_t lring, uint32_t LM,
-                                               uint32_t prm, uint32_t bits, uint32_t lane, bool act, bool has,
-                                               uint32_t opr, uint32_t lit, uint32_t lpos, uint32_t dist, bool own,
-                                               uint32_t o, uint32_t T) {
-  const uint32_t ob = o & 3u;                                      // group start within its first word
-  const uint32_t ld = lpos - opr;                                  // lring position of byte x = x + ld
-  const bool own_ = has && own;
-  const uint32_t md = own_ ? ld - dist : o - dist;                 // match source position = x + md
-  // descriptor: start, literal end | own << 31, literal delta, match delta (inactive lanes: start = T)
-  sts128(prm + lane * 16, make_uint4(opr, (opr + lit) | (own_ ? 0x80000000u : 0u), ld, md));
-  if (act) ats_or(bits + ((opr + ob) >> 5) * 4, 1u << ((opr + ob) & 31));
-  __syncwarp();
-  const uint32_t nwords = (ob + T + 3) >> 2, wbase = o >> 2;
-  uint32_t c0 = 0;                                                 // sequences starting before the row
-  for (uint32_t k0 = 0; k0 < nwords; k0 += 32) {
-    const uint4 W = lds128(bits + (k0 >> 3) * 4);                  // the row's 128 bitmap bits
-    const uint32_t p0 = __popc(W.x), p1 = __popc(W.y), p2 = __popc(W.z), p3 = __popc(W.w);
-    const uint32_t k = k0 + lane;
-    const int32_t x0 = int32_t(4 * k) - int32_t(ob);
-    if (k < nwords) {
-      const uint32_t ry = (x0 < 0 ? ob : uint32_t(x0) + ob) - 4 * k0;   // row-relative bit of the first byte in
-      const uint32_t q = ry >> 5;
-      uint32_t Wq = W.x, pre = 0;
-      Wq = q >= 1 ? W.y : Wq; pre += q >= 1 ? p0 : 0u;
-      Wq = q >= 2 ? W.z : Wq; pre += q >= 2 ? p1 : 0u;
-      Wq = q >= 3 ? W.w : Wq; pre += q >= 3 ? p2 : 0u;
-      const uint32_t j = c0 + pre + __popc(Wq & ((2u << (ry & 31)) - 1u)) - 1u;
-      const uint4 P = lds128(prm + j * 16);
-      const uint4 Q = lds128(prm + (j < 31 ? j + 1 : 31) * 16);
-      const int32_t pdst = int32_t(P.y & 0x7fffffffu);
-      const int32_t nst = j < 31 ? int32_t(Q.x) : int32_t(T);
-      const int32_t qdst = j < 31 ? int32_t(Q.y & 0x7fffffffu) : int32_t(T);
-      const int32_t xe = min(x0 + 4, int32_t(T));
-      const int32_t xs = max(x0, 0);
-      uint32_t val = lds32(ring + ((4 * (wbase + k)) & RM));   // keeps the bytes before the group (x0 < 0)
-      // four candidate segments [lo, hi) with source delta and ring; all evaluated, empty ones masked out
-      const int32_t lo4[4] = {xs, pdst, nst, qdst};
-      const int32_t hi4[4] = {pdst, nst, qdst, int32_t(T)};
-      const uint32_t dl4[4] = {P.z, P.w, Q.z, Q.w};
-      const bool fl4[4] = {true, (P.y >> 31) != 0, true, (Q.y >> 31) != 0};
-#pragma unroll
-      for (int sg = 0; sg < 4; ++sg) {
-        const int32_t s0 = max(lo4[sg], xs), s1 = min(hi4[sg], xe);
-        const uint32_t m = s0 < s1 ? byte_mask(s0 - x0, s1 - x0) : 0u;
-        const uint32_t pos = uint32_t(x0) + dl4[sg];
-        const uint32_t base = fl4[sg] ? lring : ring, msk = fl4[sg] ? LM : RM;
-        const uint32_t v = ring_word_at(base, msk, pos);
-        val = (val & ~m) | (v & m);
-      }
-      sts32(ring + ((4 * (wbase + k)) & RM), val);
-    }
-    c0 += p0 + p1 + p2 + p3;
-  }
-  // clear the bitmap words this group used, 4 per store (the group-end __syncwarp orders this before the next
-  // group's RED.OR)
-  for (uint32_t wd = 4 * lane; wd < (ob + T + 31) / 32; wd += 128) sts128(bits + wd * 4, make_uint4(0u, 0u, 0u, 0u));
-}
-
 __device__ __forceinline__ void cp_wait(uint32_t allowed) {
   if (allowed >= 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
   else if (allowed == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -1057,8 +983,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   if (wi >= a.n_blocks) return;
   const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLitRing - 1;
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(lz_smem)) + (threadIdx.x >> 5) * lz_warp_bytes(RING);
-  const uint32_t lring = ring + RING, prm = lring + kLitRing, bits = prm + kPrmBytes;
-  for (uint32_t wd = lane; wd < RING / 32; wd += 32) sts32(bits + wd * 4, 0u);
+  const uint32_t lring = ring + RING;
   const uint32_t b = a.first_block + wi;
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
@@ -1134,37 +1059,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
       const uint32_t issued = lf / kLitUnit, needed = (need + kLitUnit - 1) / kLitUnit;
       cp_wait(issued > needed ? issued - needed : 0u);
       __syncwarp();
-      bool done = false;
-      if (STRAT == GOMP_STRAT_DE) {
-        // DE rule (FORMAT.md §4): every source lies below the group start (final in the ring) or in the lane's
-        // own literal string (final in the literal ring), so every output byte of the group is a function of
-        // on-chip data that no lane of this group writes: a6 and a7 become ONE byte-parallel pass over the
-        // group's output rows, balanced over the lanes, with no inter-lane ordering at all.
-        const bool de_ok = !has || src + L <= o_carry || src >= op;
-        if (__all_sync(FULL, de_ok)) {
-          de_group_words(ring, RM, lring, LM, prm, bits, lane, act, has, ex >> 16, lit, lofs + lp, dist, src >= op,
-                         o_carry, out_sum);
-          if (STATS) {
-            const uint32_t any = __ballot_sync(FULL, has);
-            uint32_t bytes = has ? L : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) bytes += __shfl_xor_sync(FULL, bytes, d);
-            if (lane == 0) {
-              atomicAdd(stats_ptr(a) + (any ? 1 : 0), 1ull);
-              if (any) atomicAdd(stats_ptr(a) + 33 + 1, (unsigned long long)bytes);
-            }
-          }
-          done = true;
-        } else if (STATS && lane == 0) {
-          atomicAdd(stats_ptr(a) + 66, 1ull);
-        }
-      }
-      if (!done) {
-        // a6: literal strings into the output ring; a7: back-references inside the ring (MRR / SC)
-        if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
-        constexpr int S2 = STRAT == GOMP_STRAT_DE ? GOMP_STRAT_MRR : STRAT;
-        if (!resolve_group<S2, STATS>(a, ro, lane, has, dst, src, L, op, b, g0)) return;
-      }
+      // a6: literal strings into the output ring; a7: back-references inside the ring (MRR / SC)
+      if (act) ring_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+      if (!resolve_group<STRAT, STATS>(a, ro, lane, has, dst, src, L, op, b, g0)) return;
       __syncwarp();
       // flush completed 16-byte chunks to HBM (coalesced 16-byte stores), at least kFlushBytes at a time
       const uint32_t q1 = (o_carry + out_sum) >> 4;

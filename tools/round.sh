@@ -1,6 +1,6 @@
 #!/bin/bash
 # Dev helper: one GPU call producing the round's measurements under gpurun_out/ (tests, bench, reference arm,
-# ncu launch list, ncu --set full of both kernels). Usage: bash tools_round.sh <tag>
+# ncu launch list, ncu --set full of both kernels). Usage: bash tools/round.sh <tag>
 tag=${1:-r}
 python -m pytest tests -m gpu -q > gpurun_out/${tag}_gpu_tests.log 2>&1; tail -2 gpurun_out/${tag}_gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${tag}_smoke.log 2>&1; tail -1 gpurun_out/${tag}_smoke.log
