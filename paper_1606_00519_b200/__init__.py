@@ -310,3 +310,42 @@ def plan_shards(c_host, n_dev):
     first = (ctypes.c_uint32 * (n_dev + 1))()
     _check(lib().gomp_plan_shards(f.ctypes.data, len(f), n_dev, first), "gomp_plan_shards")
     return list(first)
+
+
+def decompress_sharded(c_host, devices, strategy="auto"):
+    """Decompress one file across several GPUs of this process (blocks are independent,
+    P:30-31): gomp_plan_shards splits the blocks into contiguous ranges balanced by compressed bytes; device d
+    receives the header and tables plus the payloads of its range (host->device from pinned memory on its own
+    stream) and decodes blocks [first[d], first[d+1]) with gomp_decompress_blocks. No collective, no gather:
+    returns [(first_block, CUDA uint8 tensor of that range's output)] in device order."""
+    f = _host_u8(c_host)
+    info = get_info(f)
+    devices = [torch.device(d) for d in devices]
+    first = plan_shards(f, len(devices))
+    h = torch.from_numpy(f).pin_memory()
+    bt = f[64:64 + 32 * info.n_blocks].view(np.uint32).reshape(-1, 8) if info.n_blocks else np.zeros((0, 8), np.uint32)
+    outs, pending = [], []
+    for d, dev in enumerate(devices):
+        b0, b1 = first[d], first[d + 1]
+        lo_out = min(b0 * info.block_size, info.uncompressed_len)
+        hi_out = min(b1 * info.block_size, info.uncompressed_len)
+        with torch.cuda.device(dev):
+            stream = torch.cuda.Stream(dev)
+            src = torch.zeros(info.file_len, dtype=torch.uint8, device=dev)
+            out = torch.empty(max(hi_out - lo_out, 1), dtype=torch.uint8, device=dev)
+            ws = torch.empty(workspace_size(info, max(b1 - b0, 1)), dtype=torch.uint8, device=dev)
+            with torch.cuda.stream(stream):
+                src[: info.payload_base].copy_(h[: info.payload_base], non_blocking=True)
+                if b1 > b0:
+                    p0 = int(bt[b0, 0]) | (int(bt[b0, 1]) << 32)
+                    p1 = int(bt[b1 - 1, 0]) | (int(bt[b1 - 1, 1]) << 32)
+                    p1 = min(p1 + int(bt[b1 - 1, 2]) + 16, info.file_len)
+                    src[p0:p1].copy_(h[p0:p1], non_blocking=True)
+                    decompress_into(info, src, out, ws, strategy, stream, first_block=b0, n_blocks=b1 - b0)
+            pending.append((dev, stream, ws, b0))
+            outs.append((b0, out[: hi_out - lo_out]))
+    for dev, stream, ws, b0 in pending:
+        e = read_error(ws, stream)
+        if e.status:
+            raise GompError(e.status, e.block, e.detail, where=f"decompress_sharded({dev})")
+    return outs

@@ -326,3 +326,17 @@ def test_forced_decoder_variant(kind, sub, huff):
     kw = dict(sub_blocks_per_block=sub[1], sub_block_seqs=0) if sub[0] == "k" else dict(sub_block_seqs=sub[1])
     c = gomp.compress(x, mode="bit", de=True, block_size=131072, **kw)
     _check(c, x, ["auto"], huff=huff)
+
+
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+@pytest.mark.parametrize("n_dev", [1, 2, 3])
+def test_decompress_sharded(mode, n_dev):
+    """The multi-GPU path of one process with every shard on cuda:0 (one GPU here): each shard
+    gets only the tables and its own payload range; the shard outputs, concatenated, equal the oracle's."""
+    x = _data("wiki", 1_300_007, seed=17)
+    kw = dict(sub_blocks_per_block=16, sub_block_seqs=0) if mode == "bit" else {}
+    c = gomp.compress(x, mode=mode, de=True, block_size=65536, **kw)
+    parts = gomp.decompress_sharded(c, [DEV] * n_dev)
+    assert [p[0] for p in parts] == gomp.plan_shards(c, n_dev)[:-1]
+    y = np.concatenate([p[1].cpu().numpy() for p in parts])
+    assert np.array_equal(y, oracle.decompress(c.numpy()))
