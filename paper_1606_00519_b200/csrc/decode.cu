@@ -540,7 +540,7 @@ constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per 
 constexpr size_t kSmemPerSm = 228 * 1024;   // shared memory per SM (B200)
 constexpr size_t kSmemReservedPerCta = 1024;
 // exchange area layout (bytes): [0, 8V) exit records; 768 sub-block index; 784.. per-warp aggregates
-constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912;
+constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912, kXsNext = 960;
 static_assert(8 * 32 * kHuffG <= kXsK && kHuffWarps % kHuffG == 0, "exchange area layout");
 
 __host__ __device__ constexpr uint32_t group_slot_bytes(uint32_t G, uint32_t stage_cap) {
@@ -648,14 +648,31 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       }
     } else {
       sts64(xs_s + vl * 8, exit_vl | (exit_idx << 16), e_rel);
+      // common case: every lane hands over to the next one (lane V-1 runs to the end), so every lane's true
+      // segment starts at its predecessor's exit; otherwise follow the chain from lane 0, hop by hop
+      if (lane == 0) sts32(xs_s + kXsNext + wg * 4, __all_sync(FULL, exit_vl == vl + 1) ? 1u : 0u);
+      else __all_sync(FULL, exit_vl == vl + 1);
       gsync<G>(bar);
-      uint32_t cur = 0, idx = 0, pos = 0;
-      for (uint32_t hop = 0; hop < V && cur < V; ++hop) {
-        if (vl == cur) { merged = idx; mpos = pos; }
-        const uint2 x = lds64(xs_s + cur * 8);
-        cur = x.x & 0xffffu;
-        idx = x.x >> 16;
-        pos = x.y;
+      bool next_all = true;
+      for (uint32_t w = 0; w < G; ++w) next_all &= lds32(xs_s + kXsNext + w * 4) != 0;
+      if (next_all) {
+        if (vl == 0) {
+          merged = 0;
+          mpos = 0;
+        } else {
+          const uint2 x = lds64(xs_s + (vl - 1) * 8);
+          merged = x.x >> 16;
+          mpos = x.y;
+        }
+      } else {
+        uint32_t cur = 0, idx = 0, pos = 0;
+        for (uint32_t hop = 0; hop < V && cur < V; ++hop) {
+          if (vl == cur) { merged = idx; mpos = pos; }
+          const uint2 x = lds64(xs_s + cur * 8);
+          cur = x.x & 0xffffu;
+          idx = x.x >> 16;
+          pos = x.y;
+        }
       }
     }
     const bool on = merged != 0xffffffffu;
