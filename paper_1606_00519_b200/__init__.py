@@ -331,10 +331,10 @@ def decompress_sharded(c_host, devices, strategy="auto"):
         hi_out = min(b1 * info.block_size, info.uncompressed_len)
         with torch.cuda.device(dev):
             stream = torch.cuda.Stream(dev)
-            src = torch.zeros(info.file_len, dtype=torch.uint8, device=dev)
-            out = torch.empty(max(hi_out - lo_out, 1), dtype=torch.uint8, device=dev)
-            ws = torch.empty(workspace_size(info, max(b1 - b0, 1)), dtype=torch.uint8, device=dev)
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(stream):   # allocations and copies ordered on this device's stream
+                src = torch.empty(info.file_len, dtype=torch.uint8, device=dev)
+                out = torch.empty(max(hi_out - lo_out, 1), dtype=torch.uint8, device=dev)
+                ws = torch.empty(workspace_size(info, max(b1 - b0, 1)), dtype=torch.uint8, device=dev)
                 src[: info.payload_base].copy_(h[: info.payload_base], non_blocking=True)
                 if b1 > b0:
                     p0 = int(bt[b0, 0]) | (int(bt[b0, 1]) << 32)
@@ -342,9 +342,9 @@ def decompress_sharded(c_host, devices, strategy="auto"):
                     p1 = min(p1 + int(bt[b1 - 1, 2]) + 16, info.file_len)
                     src[p0:p1].copy_(h[p0:p1], non_blocking=True)
                     decompress_into(info, src, out, ws, strategy, stream, first_block=b0, n_blocks=b1 - b0)
-            pending.append((dev, stream, ws, b0))
+            pending.append((dev, stream, ws, src))   # src stays referenced until its stream is synchronised
             outs.append((b0, out[: hi_out - lo_out]))
-    for dev, stream, ws, b0 in pending:
+    for dev, stream, ws, _ in pending:
         e = read_error(ws, stream)
         if e.status:
             raise GompError(e.status, e.block, e.detail, where=f"decompress_sharded({dev})")
