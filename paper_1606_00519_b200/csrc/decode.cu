@@ -200,6 +200,27 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait_n() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// TMA bulk copy global -> shared completed on an mbarrier (sm_90+ async proxy): one thread arms the barrier with
+// the byte count and issues the copy; every waiting thread polls the barrier's phase parity.
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  if (bytes)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+  }
+}
+
 // Window bit readers (LSB-first, RFC 1951 §3.1.1; reading R15). The decoders keep ONE register of reader state,
 // the absolute bit position `at` in the block's bitstream; window(at) returns the 64 stream bits starting there
 // as (r0, r1) from three 32-bit words and two funnel shifts. A symbol (<= 48 bits with its extra bits and its
@@ -540,7 +561,7 @@ constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per 
 constexpr size_t kSmemPerSm = 228 * 1024;   // shared memory per SM (B200)
 constexpr size_t kSmemReservedPerCta = 1024;
 // exchange area layout (bytes): [0, 8V) exit records; 768 sub-block index; 784.. per-warp aggregates
-constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912, kXsNext = 960;
+constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912, kXsNext = 960, kXsMbar = 1008;
 static_assert(8 * 32 * kHuffG <= kXsK && kHuffWarps % kHuffG == 0, "exchange area layout");
 
 __host__ __device__ constexpr uint32_t group_slot_bytes(uint32_t G, uint32_t stage_cap) {
@@ -828,6 +849,11 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   }
   const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
   const Luts t{lut_ll_s, lut_ll_s + ll_n * 4, ll_n - 1, d_n - 1, &sm};
+  // the group's stage is filled by one TMA bulk copy per sub-block, completed on this mbarrier
+  const uint32_t mbar = xs_s + kXsMbar;
+  if (vl == 0) { mbar_init(mbar, 1); fence_mbar_init(); }
+  __syncthreads();
+  uint32_t phase = 0;
   const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
   const uint32_t* subt = reinterpret_cast<const uint32_t*>(a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total) +
                          2ull * e.sub_first;
@@ -857,11 +883,17 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
       // stage [sb, sb + bsz) as 16-byte chunks (+1 chunk of window look-ahead) into the group's slot
       const uint64_t c0 = sb >> 7, nch = ((sb + bsz + 127) >> 7) - c0 + 1;
       if (nch * 16 <= stage_cap) {
-        for (uint32_t i = vl; i < nch; i += V)
-          cp_async16(stage_s + i * 16u, gbits + (c0 + i < (gmax >> 4) ? (c0 + i) * 16ull : gmax));
-        cp_commit();
-        cp_wait_n<0>();
-        gsync<G>(bar);
+        // one bulk copy of the chunks inside the readable buffer (the look-ahead chunk past it stays stale: its
+        // bits lie beyond the stream end, only window padding); earlier generic reads of the slot are ordered
+        // before the async-proxy write by the group barrier + proxy fence
+        if (vl == 0) {
+          const uint64_t lim = gmax >> 4;
+          const uint32_t nb = c0 < lim ? uint32_t(nch < lim - c0 ? nch : lim - c0) * 16u : 0u;
+          fence_proxy_async();
+          bulk_g2s(stage_s, gbits + c0 * 16ull, nb, mbar);
+        }
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
         group_sub<LONG, G>(SmemBits{stage_s, uint32_t(c0 * 128)}, t, a, vl, bar, recs_s, xs_s, b, k, uint32_t(sb),
                            bsz, rec_base + seq0, lit_base + sl, nseq, nl, last);
       } else {
