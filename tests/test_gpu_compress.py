@@ -81,3 +81,32 @@ def test_gpu_compressor_rejects_approximate_finders():
     for kw in (dict(match_finder=1), dict(max_chain=8)):
         with pytest.raises(gomp.GompError):
             gomp.compress_device(x, mode="byte", **kw)
+
+
+def test_gpu_compressor_argument_errors():
+    """C-ABI error paths of gomp_compress_device: workspace too small, destination too small, misaligned
+    buffers, bad parameters -- reported as statuses, nothing written out of bounds."""
+    import ctypes
+    x = torch.from_numpy(np.ascontiguousarray(datagen.wiki(200_000, seed=3))).to(DEV)
+    p = gomp.params(mode="bit", sub_blocks_per_block=16)
+    L = gomp.lib()
+    need = ctypes.c_size_t(0)
+    assert L.gomp_compress_device_workspace_size(x.numel(), ctypes.byref(p), ctypes.byref(need)) == 0
+    cap = L.gomp_compress_bound(x.numel(), ctypes.byref(p))
+    out = torch.empty(cap + 16, dtype=torch.uint8, device=DEV)
+    ws = torch.empty(need.value + 16, dtype=torch.uint8, device=DEV)
+    n = ctypes.c_size_t(0)
+    s0 = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def call(dst, dcap, w, wn, pp=p):
+        return L.gomp_compress_device(x.data_ptr(), x.numel(), dst, dcap, ctypes.byref(n), w, wn, ctypes.byref(pp), s0)
+
+    assert call(out.data_ptr(), cap, ws.data_ptr(), need.value - 16) == -10          # WORKSPACE_TOO_SMALL
+    assert call(out.data_ptr(), 1000, ws.data_ptr(), need.value) == -9               # DST_TOO_SMALL
+    assert call(out.data_ptr() + 1, cap, ws.data_ptr(), need.value) == -1            # misaligned destination
+    bad = gomp.params(mode="bit", sub_blocks_per_block=16)
+    bad.de_group = 48
+    assert call(out.data_ptr(), cap, ws.data_ptr(), need.value, bad) == -1           # invalid parameters
+    assert call(out.data_ptr(), cap, ws.data_ptr(), need.value) == 0
+    ref = gomp.compress(x.cpu().numpy(), p=p).numpy()
+    assert n.value == ref.size and np.array_equal(out[: n.value].cpu().numpy(), ref)

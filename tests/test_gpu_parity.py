@@ -340,3 +340,17 @@ def test_decompress_sharded(mode, n_dev):
     assert [p[0] for p in parts] == gomp.plan_shards(c, n_dev)[:-1]
     y = np.concatenate([p[1].cpu().numpy() for p in parts])
     assert np.array_equal(y, oracle.decompress(c.numpy()))
+
+
+def test_decompress_sharded_reports_device_errors():
+    """A corrupted payload in one shard's range is reported as a GompError naming that device."""
+    x = _data("wiki", 600_001, seed=19)
+    c = gomp.compress(x, mode="byte", de=True, block_size=65536).numpy().copy()
+    info = gomp.get_info(c)
+    first = gomp.plan_shards(c, 2)
+    b = first[1]                                      # first block of the second shard
+    e = c[64 + 32 * b: 64 + 32 * b + 32].view(np.uint32)
+    off = int(e[0]) | (int(e[1]) << 32)
+    c[off: off + 64] = 0xff                           # records with impossible back-references
+    with pytest.raises(gomp.GompError):
+        gomp.decompress_sharded(c, [DEV, DEV])

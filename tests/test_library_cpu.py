@@ -145,3 +145,14 @@ def test_plan_shards_balanced(n_dev):
              for d in range(n_dev)]
     avg_block = sum(sizes) / nb
     assert max(sizes) - min(sizes) <= 2 * avg_block + 1
+
+
+def test_decoder_choice_follows_the_measured_crossover():
+    """huff_variant mirrors the launcher: the speculative warp decoder from a mean of 8192 bits per sub-block
+    (profiles/r01_ncu_summary.md crossover), the thread-per-sub-block decoder below."""
+    x = datagen.matrix(400_000, seed=2)
+    for k, want in ((4, "warp"), (64, "thread")):
+        c = gomp.compress(x, mode="bit", de=True, block_size=131072, sub_blocks_per_block=k, sub_block_seqs=0)
+        info = gomp.get_info(c)
+        avg = (info.file_len - info.payload_base) * 8 / info.n_sub_total
+        assert gomp.huff_variant(info) == ("warp" if avg >= 8192 else "thread") == want, avg
