@@ -17,6 +17,7 @@ time (GB/s, 1e9); roofline_frac = (compressed + uncompressed bytes) / step time 
   C5  MatrixMarket-shaped numeric text, Bit, DE: block size x sub-blocks-per-block sweep (256 MiB per point on
       one GPU; BASELINE names 4 GiB on 8 GPUs, i.e. 512 MiB per GPU).
   f2  the GPU compressor (gomp_compress_device) beside the host compressor, identical files required.
+  f4  the paper's host-link modes at C2: "In/Out" and "In" through gomp_decompress_host.
 """
 import argparse
 import json
@@ -253,6 +254,45 @@ def run_f2(steps):
         torch.cuda.empty_cache()
 
 
+def run_f4(steps):
+    """Host-link modes of the paper at C2: "In/Out" (compressed file in, output out: the bench's e2e)
+    and "In" (compressed file in, output stays on the device), both through gomp_decompress_host with pinned
+    buffers; the copy engines' own ceiling measured beside them."""
+    kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+    x = bench.gen(kind, n, seed)
+    c = gomp.compress(x, **ckw).pin_memory()
+    info = gomp.get_info(c)
+    bufs = (torch.empty(info.file_len, dtype=torch.uint8, device=DEV),
+            torch.empty(info.uncompressed_len, dtype=torch.uint8, device=DEV),
+            torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device=DEV))
+    out_h = torch.empty(info.uncompressed_len, dtype=torch.uint8, pin_memory=True)
+    res = {}
+    for mode in ("in_out", "in"):
+        ts = []
+        for i in range(3 + steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y = gomp.decompress_host(c, out_host=out_h, device=DEV, bufs=bufs, info=info, in_mode=mode == "in")
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(time.perf_counter() - t0)
+        ok = bool(np.array_equal((y.cpu() if y.is_cuda else y).numpy(), x))
+        res[mode] = (round(n / statistics.median(ts) / 1e9, 2), ok)
+    h2d = torch.empty(info.file_len, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(info.file_len, dtype=torch.uint8, device=DEV)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        d.copy_(h2d, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_gbs = 5 * info.file_len / (time.perf_counter() - t0) / 1e9
+    print(json.dumps({"config": "f4-C2", "in_out_gbs": res["in_out"][0], "in_gbs": res["in"][0],
+                      "h2d_copy_gbs": round(h2d_gbs, 1), "in_mode_ceiling_gbs": round(h2d_gbs * n / info.file_len, 1),
+                      "parity": res["in_out"][1] and res["in"][1],
+                      "note": "uncompressed GB/s through gomp_decompress_host, wall clock incl. synchronisation"}),
+          flush=True)
+
+
 def main():
     global FLUSH
     ap = argparse.ArgumentParser()
@@ -263,7 +303,7 @@ def main():
         raise SystemExit("bench_configs.py needs a CUDA device (no CPU fallback)")
     FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device=DEV)
     for name in args.only.split(","):
-        {"C1": run_c1, "C3": run_c3, "C4": run_c4, "C5": run_c5, "f2": run_f2}[name](args.steps)
+        {"C1": run_c1, "C3": run_c3, "C4": run_c4, "C5": run_c5, "f2": run_f2, "f4": run_f4}[name](args.steps)
 
 
 if __name__ == "__main__":

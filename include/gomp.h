@@ -199,6 +199,9 @@ gomp_status gomp_decompress_blocks(const gomp_info* info, uint32_t first_block, 
  * host->device copy of h_src (pinned memory for asynchrony) into d_src_buf, the decompression, and the
  * device->host copy of the output into h_dst. Caller synchronises the stream before reading h_dst.
  * d_src_buf >= src_len bytes, d_dst_buf >= uncompressed_len bytes (16-byte aligned), workspace as above.
+ * h_dst = NULL selects the paper's "In" mode: the output stays in d_dst_buf (dst_cap is then ignored).
+ * The blocks are cut into chunks of doubling size; each chunk's copy-in, kernels (on internal streams) and
+ * copy-out overlap with the other chunks'.
  */
 gomp_status gomp_decompress_host(const gomp_info* info, const uint8_t* h_src, size_t src_len, uint8_t* h_dst,
                                  size_t dst_cap, uint8_t* d_src_buf, uint8_t* d_dst_buf, void* d_workspace,

@@ -282,9 +282,12 @@ def decompress(c, out=None, strategy="auto", stream=None, info=None, check=True,
     return y
 
 
-def decompress_host(c_host, out_host=None, strategy="auto", device=None, stream=None, bufs=None, info=None):
+def decompress_host(c_host, out_host=None, strategy="auto", device=None, stream=None, bufs=None, info=None,
+                    in_mode=False):
     """End-to-end path (gomp_decompress_host): host (pinned) compressed file -> host output, with the copies
-    enqueued on the stream. Returns the host output tensor (synchronised, error-checked)."""
+    enqueued on the stream. Returns the host output tensor (synchronised, error-checked). in_mode=True is the
+    paper's "In" mode: only the compressed file crosses the host link, the output stays on the
+    device and the device tensor is returned."""
     device = torch.device(device or "cuda")
     info = info or get_info(c_host)
     if out_host is None:
@@ -295,13 +298,14 @@ def decompress_host(c_host, out_host=None, strategy="auto", device=None, stream=
                 torch.empty(workspace_size(info), dtype=torch.uint8, device=device))
     d_src, d_dst, ws = bufs
     sp = _stream_ptr(stream, device)
-    _check(lib().gomp_decompress_host(ctypes.byref(info), c_host.data_ptr(), c_host.numel(), out_host.data_ptr(),
-                                      out_host.numel(), d_src.data_ptr(), d_dst.data_ptr(), ws.data_ptr(), ws.numel(),
+    _check(lib().gomp_decompress_host(ctypes.byref(info), c_host.data_ptr(), c_host.numel(),
+                                      None if in_mode else out_host.data_ptr(), 0 if in_mode else out_host.numel(),
+                                      d_src.data_ptr(), d_dst.data_ptr(), ws.data_ptr(), ws.numel(),
                                       _strategy(strategy, False), sp), "gomp_decompress_host")
     e = read_error(ws, stream)
     if e.status:
         raise GompError(e.status, e.block, e.detail, where="gomp_decompress_host")
-    return out_host[: info.uncompressed_len]
+    return d_dst[: info.uncompressed_len] if in_mode else out_host[: info.uncompressed_len]
 
 
 def plan_shards(c_host, n_dev):

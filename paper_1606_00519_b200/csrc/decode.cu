@@ -1609,9 +1609,9 @@ struct Pipe {
 GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_t* h_src, size_t src_len, uint8_t* h_dst,
                                              size_t dst_cap, uint8_t* d_src_buf, uint8_t* d_dst_buf, void* d_ws,
                                              size_t ws_bytes, int strategy, void* stream) {
-  if (!info || !h_src || !d_src_buf || !d_ws || (!h_dst && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
+  if (!info || !h_src || !d_src_buf || !d_ws || (!d_dst_buf && info->uncompressed_len)) return GOMP_ERR_INVALID_ARG;
   if (src_len < info->file_len) return GOMP_ERR_TRUNCATED;
-  if (dst_cap < info->uncompressed_len) return GOMP_ERR_DST_TOO_SMALL;
+  if (h_dst && dst_cap < info->uncompressed_len) return GOMP_ERR_DST_TOO_SMALL;   // h_dst NULL: "In" mode
   size_t need = 0;
   gomp_decompress_workspace_size(info, 0, &need);
   if (ws_bytes < need) return GOMP_ERR_WORKSPACE_TOO_SMALL;
@@ -1671,7 +1671,7 @@ GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_
                                            strategy, cs, false, b0);
     if (s != GOMP_OK) return s;
     if (cudaEventRecord(ec, cs) != cudaSuccess || cudaStreamWaitEvent(p.d2h, ec, 0) != cudaSuccess) return GOMP_ERR_CUDA;
-    if (o1 > o0 && cudaMemcpyAsync(h_dst + o0, d_dst_buf + o0, o1 - o0, cudaMemcpyDeviceToHost, p.d2h) != cudaSuccess)
+    if (h_dst && o1 > o0 && cudaMemcpyAsync(h_dst + o0, d_dst_buf + o0, o1 - o0, cudaMemcpyDeviceToHost, p.d2h) != cudaSuccess)
       return GOMP_ERR_CUDA;
   }
   cudaEvent_t ee = p.event();

@@ -226,13 +226,16 @@ def test_host_end_to_end():
 @pytest.mark.parametrize("mode", ["byte", "bit"])
 @pytest.mark.parametrize("n,bs", [(700_001, 16384), (3_000_017, 8192), (100_000, 65536), (0, 65536)])
 def test_host_pipeline(mode, n, bs):
-    """gomp_decompress_host cuts the blocks into up to 8 chunks (>= 64 blocks each) whose copies and kernels
-    overlap on internal streams; output must equal the input, for every chunk count including one."""
+    """gomp_decompress_host cuts the blocks into chunks of doubling size whose copies and kernels overlap on
+    internal streams; output must equal the input, for every chunk count including one, in the "In/Out" mode
+    and in the "In" mode (h_dst NULL: the output stays on the device)."""
     x = datagen.wiki(n, seed=17)
     c = gomp.compress(x, mode=mode, block_size=bs).pin_memory()
     for strategy in ("auto", "mrr"):
         y = gomp.decompress_host(c, device=DEV, strategy=strategy)
         assert np.array_equal(y.numpy(), x)
+        z = gomp.decompress_host(c, device=DEV, strategy=strategy, in_mode=True)
+        assert z.is_cuda and np.array_equal(z.cpu().numpy(), x)
 
 
 def test_host_pipeline_reports_late_error():
