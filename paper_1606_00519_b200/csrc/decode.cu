@@ -1339,13 +1339,14 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     if (fast) {
       // a6: literal string of each sequence from the literal ring into the output ring
       if (act && lit) or_copy(ring, RM, op, lring, LM, lofs + lp, lit);
-      // a7 (DE, one round): named barrier w (64 threads) passes warp w-1's "done" to warp w; a warp that needs
-      // nothing from the batch copies first and consumes the barrier afterwards, so its own "done" still
-      // implies all earlier ones
-      const bool need = __any_sync(FULL, has && src < op && src + L > oB);
-      if (w > 0 && need) chain_sync(w);
-      if (has) or_copy(ring, RM, dst, ring, RM, src, L);
-      if (w > 0 && !need) chain_sync(w);
+      // a7 (DE, one round): named barrier w (64 threads) passes warp w-1's "done" to warp w. Only the lanes whose
+      // source overlaps output of this batch (written by earlier warps) copy after the barrier; the others copy
+      // before it, so the chain's critical path holds only those copies, and each warp's "done" still implies
+      // all earlier ones
+      const bool inb = has && src < op && src + L > oB;
+      if (has && !inb) or_copy(ring, RM, dst, ring, RM, src, L);
+      if (w > 0) chain_sync(w);
+      if (inb) or_copy(ring, RM, dst, ring, RM, src, L);
       if (w + 1 < kBW) chain_arrive(w + 1);
       // zero the next batch's range (beyond everything this batch writes or reads)
       const uint32_t zt = (oB + OT + kLzBatchMaxOut + 15u) & ~15u;

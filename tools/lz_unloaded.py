@@ -1,0 +1,15 @@
+"""Dev helper: LZ77 kernel alone on the first n blocks of C2 (unloaded SMs), for an ncu source-level capture."""
+import sys
+sys.path.insert(0, '.')
+import torch, bench, paper_1606_00519_b200 as gomp
+kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+x = bench.gen(kind, n, seed)
+c = gomp.compress(x, **ckw)
+info = gomp.get_info(c)
+d = c.cuda(); out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device="cuda")
+ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device="cuda")
+nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+gomp.decompress_into(info, d, out, ws, phase="decode", n_blocks=nb)
+for _ in range(3):
+    gomp.decompress_into(info, d, out, ws, phase="lz77", n_blocks=nb)
+torch.cuda.synchronize()
