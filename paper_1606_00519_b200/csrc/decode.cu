@@ -29,7 +29,11 @@ namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t kPipeStreams = 4;     // compute streams of the pipelined host path
-constexpr uint32_t kPipeMaxChunks = 12;  // chunks of the pipelined host path (sizes double: small first chunks)
+constexpr uint32_t kPipeMaxChunks = 12;
+#ifndef GOMP_LOWLAT_CTAS_PER_SM
+#define GOMP_LOWLAT_CTAS_PER_SM 3
+#endif
+constexpr uint32_t kLowLatCtasPerSm = GOMP_LOWLAT_CTAS_PER_SM;   // LZ77 grids up to this many CTAs per SM use or_copy_ll  // chunks of the pipelined host path (sizes double: small first chunks)
 constexpr int kLz77Warps = 2;        // warps (= data blocks) per CTA of the LZ77 kernel
 constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
 
@@ -1224,7 +1228,39 @@ __device__ __forceinline__ void or_copy(uint32_t D, uint32_t dm, uint32_t d, uin
   if (p == last) ats_or(D + (p & dm), __funnelshift_r(lo, ldsw(S + ((sa + 4) & sm)), sh) & mlast);
 }
 
-template <bool STATS>
+// Latency variant of or_copy for grids that leave SMs idle: 16 destination bytes per step, the five source words of
+// a step loaded before any store and every destination word OR-ed in (masked; zero beyond the copy), so a copy of
+// up to 13 bytes costs one shared-memory round trip and no branch. It spends more shared atomics per byte, which
+// loses under full load (measured: one C2 block 0.33 vs 0.41 ms; 1024 blocks 0.74 vs 0.60 ms).
+__device__ __forceinline__ void or_copy_ll(uint32_t D, uint32_t dm, uint32_t d, uint32_t S, uint32_t sm, uint32_t s,
+                                           uint32_t n) {
+  const uint32_t e = d + n, first = d & ~3u, last = (e - 1) & ~3u, sh = ((s - d) & 3u) * 8u;
+  const uint32_t mfirst = 0xffffffffu << ((d & 3u) * 8u), mlast = 0xffffffffu >> ((3u - ((e - 1) & 3u)) * 8u);
+  uint32_t sa = (s - (d & 3u)) & ~3u, lo = ldsw(S + (sa & sm));
+  for (uint32_t p = first; p <= last; p += 16, sa += 16) {
+    uint32_t w[5];
+    w[0] = lo;
+#pragma unroll
+    for (int k = 1; k < 5; ++k) w[k] = ldsw(S + ((sa + 4 * k) & sm));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t q = p + 4 * k;
+      uint32_t m = q <= last ? 0xffffffffu : 0u;
+      if (q == first) m &= mfirst;
+      if (q == last) m &= mlast;
+      ats_or(D + (q & dm), __funnelshift_r(w[k], w[k + 1], sh) & m);
+    }
+    lo = w[4];
+  }
+}
+template <bool LOWLAT>
+__device__ __forceinline__ void ring_copy(uint32_t D, uint32_t dm, uint32_t d, uint32_t S, uint32_t sm, uint32_t s,
+                                          uint32_t n) {
+  if (LOWLAT) or_copy_ll(D, dm, d, S, sm, s, n);
+  else or_copy(D, dm, d, S, sm, s, n);
+}
+
+template <bool STATS, bool LOWLAT>
 __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t bz[];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1338,15 +1374,15 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     }
     if (fast) {
       // a6: literal string of each sequence from the literal ring into the output ring
-      if (act && lit) or_copy(ring, RM, op, lring, LM, lofs + lp, lit);
+      if (act && lit) ring_copy<LOWLAT>(ring, RM, op, lring, LM, lofs + lp, lit);
       // a7 (DE, one round): named barrier w (64 threads) passes warp w-1's "done" to warp w. Only the lanes whose
       // source overlaps output of this batch (written by earlier warps) copy after the barrier; the others copy
       // before it, so the chain's critical path holds only those copies, and each warp's "done" still implies
       // all earlier ones
       const bool inb = has && src < op && src + L > oB;
-      if (has && !inb) or_copy(ring, RM, dst, ring, RM, src, L);
+      if (has && !inb) ring_copy<LOWLAT>(ring, RM, dst, ring, RM, src, L);
       if (w > 0) chain_sync(w);
-      if (inb) or_copy(ring, RM, dst, ring, RM, src, L);
+      if (inb) ring_copy<LOWLAT>(ring, RM, dst, ring, RM, src, L);
       if (w + 1 < kBW) chain_arrive(w + 1);
       // zero the next batch's range (beyond everything this batch writes or reads)
       const uint32_t zt = (oB + OT + kLzBatchMaxOut + 15u) & ~15u;
@@ -1540,12 +1576,22 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   switch (s) {
     case GOMP_STRAT_DE: {
       const size_t smem = lzb_smem_bytes(a.ring_bytes);
+      // a grid of at most one CTA per SM leaves the SMs latency-bound: the low-latency copies win there
+      static int n_sm = 0;
+      if (!n_sm) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+          n_sm = 1;
+      }
       if (stats) {
-        cudaFuncSetAttribute(lz77_batch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        lz77_batch_kernel<true><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
+        cudaFuncSetAttribute(lz77_batch_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        lz77_batch_kernel<true, false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
+      } else if (nblk <= uint32_t(n_sm) * kLowLatCtasPerSm) {
+        cudaFuncSetAttribute(lz77_batch_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        lz77_batch_kernel<false, true><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
       } else {
-        cudaFuncSetAttribute(lz77_batch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        lz77_batch_kernel<false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
+        cudaFuncSetAttribute(lz77_batch_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        lz77_batch_kernel<false, false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
       }
       break;
     }

@@ -11,7 +11,7 @@ for path in [gomp.LIB_PATH] + sorted(glob.glob("exp/*.so")):
     d = c.cuda(); out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device="cuda")
     ws = torch.empty(gomp.workspace_size(info), dtype=torch.uint8, device="cuda")
     r = {}
-    for nb in (8, 1024):
+    for nb in [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else '8,1024').split(',')]:
         gomp.decompress_into(info, d, out, ws, phase="decode", n_blocks=nb)
         ts = []
         for _ in range(10):
