@@ -215,6 +215,31 @@ def test_blocks_range_and_shards():
         assert np.array_equal(np.concatenate(parts), x)
 
 
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+def test_lz77_copy_variants(mode):
+    """The DE LZ77 kernel has two copy variants chosen by grid size (grids of <= 3 CTAs per SM take
+    the latency variant): the same 600-block file decoded whole (throughput variant) and in 64-block ranges
+    (latency variant) must both equal the input and the oracle."""
+    x = datagen.wiki(600 * 65536 - 777, seed=12)
+    c = gomp.compress(x, mode=mode, de=True, block_size=65536, sub_blocks_per_block=8)
+    info = gomp.get_info(c)
+    assert info.n_blocks == 600
+    assert np.array_equal(_gpu(c).cpu().numpy(), x)
+    d = c.to(DEV)
+    out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device=DEV)
+    ws = torch.empty(gomp.workspace_size(info, 64), dtype=torch.uint8, device=DEV)
+    for b0 in range(0, 600, 64):
+        nb = min(64, 600 - b0)
+        gomp.decompress_into(info, d, out[b0 * 65536:], ws, first_block=b0, n_blocks=nb)
+        assert gomp.read_error(ws).status == 0
+    y = out.cpu().numpy()
+    assert np.array_equal(y, x)
+    cn = c.numpy()
+    for b in (0, 317, 599):
+        ref = oracle.decompress_blocks(cn, b, b + 1, 65536)
+        assert np.array_equal(y[b * 65536: b * 65536 + len(ref)], ref)
+
+
 def test_host_end_to_end():
     x = datagen.wiki(2_000_000, seed=7)
     for mode in ("byte", "bit"):
@@ -273,7 +298,7 @@ def test_bad_arguments():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C3-byte-mrr", "C3-bit-de"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3-byte-mrr", "C3-byte-de", "C3-bit-de"])
 def test_full_size_configs(cfg):
     """BASELINE.json configs at full size, in the launch configuration bench.py times: every output byte vs
     the original input, and the oracle on sampled blocks."""
@@ -286,6 +311,9 @@ def test_full_size_configs(cfg):
     elif cfg == "C3-byte-mrr":
         x = datagen.nested(256 << 20, 8, seed=3)
         c = gomp.compress(x, mode="byte", de=False, block_size=262144)
+    elif cfg == "C3-byte-de":
+        x = datagen.nested(256 << 20, 8, seed=3)
+        c = gomp.compress(x, mode="byte", de=True, block_size=262144)
     else:
         x = datagen.nested(256 << 20, 8, seed=3)
         c = gomp.compress(x, mode="bit", de=True, block_size=262144, sub_block_seqs=16)
