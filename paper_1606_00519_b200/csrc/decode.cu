@@ -1178,7 +1178,8 @@ constexpr uint32_t kLzLUnit = 32 * kBW * 16;  // literal prefetch unit: one 16-b
 constexpr uint32_t kLzBatchMaxOut = 4096;   // fast path: batch output bytes = zero-ahead distance
 constexpr uint32_t kLzFlush = 4096;         // ring -> HBM flush granularity
 // batch tables after the ring: literal ring | per-warp group totals (u32 each) | per-warp flags
-constexpr uint32_t kLzTab = kLzLR, kLzFlg = kLzTab + 16, kLzEnd = kLzFlg + kBW * 4;
+// group totals and flags of a batch, double-buffered by batch parity (one CTA barrier per batch)
+constexpr uint32_t kLzTab = kLzLR, kLzFlg = kLzTab + 32, kLzEnd = kLzFlg + 32;
 
 __host__ __device__ constexpr uint32_t lzb_smem_bytes(uint32_t ring) { return ring + kLzEnd; }
 
@@ -1261,7 +1262,7 @@ __device__ __forceinline__ void ring_copy(uint32_t D, uint32_t dm, uint32_t d, u
 }
 
 template <bool STATS, bool LOWLAT>
-__global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int byte_mode) {
+__global__ void __launch_bounds__(32 * kBW, 8) lz77_batch_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t bz[];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
@@ -1323,7 +1324,23 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
     const uint32_t incl = warp_incl_scan_u32(v, lane);
     const uint32_t tot = __shfl_sync(FULL, incl, 31);
     const uint32_t ex = incl - v;
-    if (lane == 0) sts32(tab + w * 4, tot);
+    // group-local checks, published with the totals so that ONE barrier makes every decision uniform:
+    // 1 = malformed record (reported here), 2 = the group breaks the DE rule (its source neither precedes the
+    // group nor lies in the sequence's own literals; R2/A4), 4 = a source may precede the block (exact test below)
+    const bool has = act && L;
+    const bool lbad = act && (L ? (dist < L || dist > a.window) : (r >> 16) != 0);
+    const bool any_lbad = __any_sync(FULL, lbad);
+    const bool de_ok = __all_sync(FULL, !has || dist >= (ex >> 16) + lit + L || dist <= lit);
+    const bool maybe_neg = __any_sync(FULL, has && dist > oB + (ex >> 16) + lit);
+    const uint32_t par = (B0 / kBW) & 1u, tabk = tab + par * 16, flgk = flg + par * 16;
+    if (lane == 0) {
+      sts32(tabk + w * 4, tot);
+      sts32(flgk + w * 4, (any_lbad ? 1u : 0u) | (de_ok ? 0u : 2u) | (maybe_neg ? 4u : 0u));
+    }
+    if (any_lbad) {
+      const bool any_rec = __any_sync(FULL, act && !L && (r >> 16) != 0);
+      if (lane == 0) report(a, any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
+    }
     __syncthreads();
     // flush the completed output of earlier batches (final after the barrier), at least kFlushBytes at a time
     if (oB >= flushed + kLzFlush + 16) {
@@ -1333,38 +1350,33 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
       flushed = q1 * 16;
     }
     // batch offsets (all warps compute all of them); group totals are (out << 16 | lit), each half < 2^16
-    const uint4 T4 = lds128(tab);
+    const uint4 T4 = lds128(tabk), F4 = lds128(flgk);
     static_assert(kBW == 4, "batch offsets from one 16-byte load");
+    const uint32_t fl = F4.x | F4.y | F4.z | F4.w;
     const uint32_t o0 = T4.x >> 16, o1 = T4.y >> 16, o2 = T4.z >> 16, o3 = T4.w >> 16;
     const uint32_t l0 = T4.x & 0xffffu, l1 = T4.y & 0xffffu, l2 = T4.z & 0xffffu, l3 = T4.w & 0xffffu;
     const uint32_t OT = o0 + o1 + o2 + o3, LT = l0 + l1 + l2 + l3;
+    if (fl & 1u) return;                                       // device error already reported
+    if (oB + OT > ulen || lB + LT > e.n_lit) {                 // more output or literals than the block holds
+      if (threadIdx.x == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, uint64_t(B0) * 32);
+      return;
+    }
     const uint32_t ob_w = w == 0 ? 0u : w == 1 ? o0 : w == 2 ? o0 + o1 : o0 + o1 + o2;
     const uint32_t lb_w = w == 0 ? 0u : w == 1 ? l0 : w == 2 ? l0 + l1 : l0 + l1 + l2;
     const uint32_t og = oB + ob_w, lg = lB + lb_w;
-    const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
     const uint32_t op = og + (ex >> 16), lp = lg + (ex & 0xffffu), dst = op + lit, src = dst - dist;
-    const bool has = act && L;
-    const bool bad_lane = act && (L ? (dist < L || dist > a.window || dist > dst) : (r >> 16) != 0);
-    const bool bad_sz = og + out_sum > ulen || lg + lit_sum > e.n_lit;
-    const bool any_bad = __any_sync(FULL, bad_lane) || bad_sz;
-    const bool de_ok = __all_sync(FULL, !has || src + L <= og || src >= op);
-    const uint32_t myfl = (any_bad ? 1u : 0u) | (de_ok ? 0u : 2u);
-    if (lane == 0) sts32(flg + w * 4, myfl);
-    if (any_bad) {
-      const bool any_rec = __any_sync(FULL, act && !L && (r >> 16) != 0);
-      if (lane == 0) report(a, bad_sz || any_rec ? GOMP_ERR_CORRUPT_STREAM : GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
+    if (fl & 4u) {                                             // rare (the block's first window): exact test
+      const bool neg = has && dist > dst;
+      if (__syncthreads_or(neg)) {
+        if (__any_sync(FULL, neg) && lane == 0) report(a, GOMP_ERR_MALFORMED_BACKREF, b, g * 32);
+        return;
+      }
     }
     // fast path: the batch fits the zero-ahead distance, its literals have landed, and the ring holds the
     // window, this batch and the next batch's zeroed range without touching unflushed output
     const uint32_t landed = lf > 2 * kLzLUnit ? lf - 2 * kLzLUnit : 0u;
     const bool room = OT <= kLzBatchMaxOut && a.window + 2 * kLzBatchMaxOut <= RING &&
                       oB + OT + kLzBatchMaxOut - flushed <= RING;
-    uint32_t fl = 0;
-    if (__syncthreads_or(myfl != 0)) {
-#pragma unroll
-      for (uint32_t ww = 0; ww < kBW; ++ww) fl |= lds32(flg + ww * 4);
-    }
-    if (fl & 1u) return;                                       // device error already reported
     bool fast = !(fl & 2u) && room && lofs + lB + LT <= landed;
     if (!fast && !(fl & 2u) && room && lofs + lB + LT <= lf) {
       // the batch's literals are issued but maybe still in flight: wait for all of them (uniform, rare)
@@ -1408,7 +1420,7 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
         for (uint32_t ww = 0; ww < kBW; ++ww) {
           const uint32_t gg = B0 + ww, ii = gg * 32 + lane;
           if (gg >= ngroups) break;
-          if (STATS && lane == 0 && (lds32(flg + ww * 4) & 2u)) atomicAdd(stats_ptr(a) + 66, 1ull);
+          if (STATS && lane == 0 && (lds32(flgk + ww * 4) & 2u)) atomicAdd(stats_ptr(a) + 66, 1ull);
           const bool act2 = ii < n_seq;
           const uint32_t r2 = act2 ? __ldg(recs + ii) : 0u;
           const uint32_t lit2 = r2 & 1023u, mc2 = (r2 >> 10) & 63u, dist2 = (r2 >> 16) + 1u;
@@ -1419,7 +1431,7 @@ __global__ void __launch_bounds__(32 * kBW) lz77_batch_kernel(const Args a, int 
           if (!resolve_group<GOMP_STRAT_MRR, STATS>(a, go, lane, act2 && L2, dst2, dst2 - dist2, L2, op2, b, gg * 32))
             break;
           __syncwarp();
-          const uint32_t tu = lds32(tab + ww * 4);
+          const uint32_t tu = lds32(tabk + ww * 4);
           og2 += tu >> 16;
           lg2 += tu & 0xffffu;
         }
