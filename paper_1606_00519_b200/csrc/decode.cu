@@ -48,6 +48,8 @@ struct Args {
   uint64_t total, file_len, payload_base, tok_stride;
   uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, ll_bits, d_bits, max_tok;
   uint32_t n_sub_total, nb_total, ring_bytes;
+  // K1b split grid: CTAs from split_first on take 1/split_parts of a block's sub-blocks each
+  uint32_t split_first, split_parts;
 };
 
 // ------------------------------------------------------------------ completion: error word (a9)
@@ -840,12 +842,21 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint32_t grp = warp / G, vl = tid % V, bar = 1 + grp;
   const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + d_n)) + grp * group_slot_bytes(G, stage_cap);
   const uint32_t recs_s = slot_s, xs_s = slot_s + V * kRec, stage_s = xs_s + kXsBytes;
-  const uint32_t bi = blockIdx.x, b = a.first_block + bi;
+  // in a split grid each CTA takes only a share of a block's sub-blocks (launcher)
+  uint32_t bi = blockIdx.x, part = 0, parts = 1;
+  if (bi >= a.split_first) {
+    const uint32_t j = bi - a.split_first;
+    parts = a.split_parts;
+    bi = a.split_first + j / parts;
+    part = j % parts;
+  }
+  const uint32_t b = a.first_block + bi;
   const BlockEntry e = load_entry(a.src, b, lane);
   if (!huff_block_ok(a, e, block_ulen(a, b))) {
     if (tid == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
     return;
   }
+  const uint32_t k_lo = part * e.n_sub / parts, k_hi = (part + 1) * e.n_sub / parts;
   const uint8_t* pl = a.src + e.payload_off;
   if (!build_tables<LONG>(sm, lut_ll, lut_d, pl, a)) {
     if (tid == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
@@ -867,10 +878,10 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
   const uint8_t* gbits = pl + kTreeBytes;
   for (;;) {
-    if (vl == 0) sts32(xs_s + kXsK, atomicAdd(&sm.next, 1u));
+    if (vl == 0) sts32(xs_s + kXsK, k_lo + atomicAdd(&sm.next, 1u));
     gsync<G>(bar);
     const uint32_t k = lds32(xs_s + kXsK);
-    if (k >= e.n_sub) break;
+    if (k >= k_hi) break;
     // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
     uint64_t sb = 0;
     uint32_t sl = 0;
@@ -1483,6 +1494,16 @@ void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
 
 // reset_ws: clear the error word / statistics first (a pipelined caller clears them once); tok_block0: block
 // slot of the workspace token buffer used for block `first` (pipelined chunks in flight use disjoint slots)
+// SMs of the current device (cached per process; one device type per node)
+uint32_t sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0, v = 0;
+    n = cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0 ? v : 1;
+  }
+  return uint32_t(n);
+}
+
 gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
                              size_t src_len, uint8_t* d_dst, size_t dst_cap, void* d_ws, size_t ws_bytes,
                              int strategy, cudaStream_t st, bool reset_ws = true, uint32_t tok_block0 = 0) {
@@ -1533,6 +1554,8 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   a.n_sub_total = info->n_sub_total;
   a.nb_total = info->n_blocks;
   a.ring_bytes = 16384;
+  a.split_first = nblk;   // no K1b split grid unless the launcher sets one
+  a.split_parts = 1;
   while (a.ring_bytes < info->window_size + 2 * kLzBatchMaxOut) a.ring_bytes <<= 1;
   const bool byte_mode = info->mode == GOMP_MODE_BYTE;
   if (!byte_mode && !lz77_only) {
@@ -1561,13 +1584,22 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       const uint64_t fit = (kSmemMax - tabs) / slot;
       const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / kHuffG, fit, avg_sub})));
       const size_t smem = tabs + ngr * slot;
-      if (LONGc) {
-        cudaFuncSetAttribute(huff_warp_kernel<true, kHuffG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<true, kHuffG><<<nblk, 32 * kHuffG * ngr, smem, st>>>(a, cap);
-      } else {
-        cudaFuncSetAttribute(huff_warp_kernel<false, kHuffG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        huff_warp_kernel<false, kHuffG><<<nblk, 32 * kHuffG * ngr, smem, st>>>(a, cap);
+      const auto kern = LONGc ? huff_warp_kernel<true, kHuffG> : huff_warp_kernel<false, kHuffG>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      // split grid: blocks that fill at most half of the resident CTA slots are each decoded by two CTAs taking
+      // half of its sub-blocks (the idle slots would otherwise wait out whole-block latencies; measured on the
+      // first 74 blocks of C2: 0.095 vs 0.149 ms). Splitting only the last partial wave of a large grid was
+      // measured as no gain (C2: 0.674 vs 0.675 ms).
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, int(32 * kHuffG * ngr), smem) != cudaSuccess) occ = 0;
+      const uint32_t slots = uint32_t(std::max(occ, 0)) * sm_count();
+      uint32_t grid = nblk;
+      if (2 * uint64_t(nblk) <= slots && avg_sub >= 2 * uint64_t(ngr)) {
+        a.split_first = 0;
+        a.split_parts = 2;
+        grid = 2 * nblk;
       }
+      kern<<<grid, 32 * kHuffG * ngr, smem, st>>>(a, cap);
     } else {
       // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block, rounds
       // of nt sub-blocks staged together
@@ -1589,16 +1621,10 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     case GOMP_STRAT_DE: {
       const size_t smem = lzb_smem_bytes(a.ring_bytes);
       // a grid of at most one CTA per SM leaves the SMs latency-bound: the low-latency copies win there
-      static int n_sm = 0;
-      if (!n_sm) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-          n_sm = 1;
-      }
       if (stats) {
         cudaFuncSetAttribute(lz77_batch_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         lz77_batch_kernel<true, false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
-      } else if (nblk <= uint32_t(n_sm) * kLowLatCtasPerSm) {
+      } else if (nblk <= sm_count() * kLowLatCtasPerSm) {
         cudaFuncSetAttribute(lz77_batch_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         lz77_batch_kernel<false, true><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
       } else {
