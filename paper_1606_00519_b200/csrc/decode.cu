@@ -130,6 +130,7 @@ struct CanonTab {        // canonical code description of one table (RFC 1951 §
   uint16_t first[16];
   uint16_t index[16];
   uint16_t running[16];
+  uint32_t lim[16];      // (first[l] + count[l]) << (16 - l): non-decreasing in l; lim[0] = 0
 };
 
 struct HuffSmem {
@@ -331,12 +332,14 @@ __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, co
         int left = 1;
         uint32_t first = 0, index = 0;
         T.count[0] = 0;
+        T.lim[0] = 0;
         for (int l = 1; l <= 15; ++l) {
           left = (left << 1) - T.count[l];
           if (left < 0) badl = 1;                        // over-subscribed code set
           first = l == 1 ? 0u : (first + T.count[l - 1]) << 1;
           T.first[l] = uint16_t(first);
           T.index[l] = uint16_t(index);
+          T.lim[l] = (first + T.count[l]) << (16 - l);
           index += T.count[l];
         }
       }
@@ -361,16 +364,21 @@ __device__ bool build_tables(HuffSmem& sm, uint32_t* lut_ll, uint32_t* lut_d, co
   if (sm.bad) return false;
   // canonical decode of the code at the head of `bits` (nb valid index bits, first stream bit = bit 0) with
   // table t: symbol | length << 16, or 0xffffffff when no code of length <= nb matches
+  // The length L of the head code is the smallest l with v16 < lim[l] (left-justified canonical limits are
+  // non-decreasing), found by a 4-step binary search; bits past nb are zero and only matter when L > nb.
   auto canon = [&](int t, uint32_t bits, uint32_t nb) -> uint32_t {
-    const uint32_t v = nb ? __brev(bits) >> (32 - nb) : 0u;   // code bits, first stream bit most significant
+    const uint32_t v16 = __brev(bits) >> 16;   // code bits, first stream bit most significant, left-justified
     const CanonTab& T = sm.tab[t];
-    for (uint32_t l = 1; l <= nb; ++l) {
-      const uint32_t code = v >> (nb - l);
-      if (code - T.first[l] < T.count[l])
-        return uint32_t(t ? sm.sorted_d[T.index[l] + code - T.first[l]] : sm.sorted_ll[T.index[l] + code - T.first[l]]) |
-               (l << 16);
-    }
-    return 0xffffffffu;
+    uint32_t l = 0;                            // largest l in [0, 15] with lim[l] <= v16
+#pragma unroll
+    for (uint32_t step = 8; step; step >>= 1)
+      if (l + step <= 15 && T.lim[l + step] <= v16) l += step;
+    const uint32_t L = l + 1;
+    if (L > nb) return 0xffffffffu;
+    const uint32_t code = v16 >> (16 - L);
+    if (code - T.first[L] >= T.count[L]) return 0xffffffffu;
+    return uint32_t(t ? sm.sorted_d[T.index[L] + code - T.first[L]] : sm.sorted_ll[T.index[L] + code - T.first[L]]) |
+           (L << 16);
   };
   for (uint32_t i = tid; i < ll_n + d_n; i += blockDim.x) {
     const int t = i >= ll_n;
