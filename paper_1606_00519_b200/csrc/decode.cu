@@ -1280,12 +1280,14 @@ __device__ __forceinline__ void ring_copy(uint32_t D, uint32_t dm, uint32_t d, u
   else or_copy(D, dm, d, S, sm, s, n);
 }
 
-template <bool STATS, bool LOWLAT>
+// RC: the output ring size when known at compile time (the default window's 16 KiB ring; 0 = a.ring_bytes),
+// so the ring masks and the offsets of the literal ring and batch tables are immediates
+template <bool STATS, bool LOWLAT, uint32_t RC>
 __global__ void __launch_bounds__(32 * kBW, 8) lz77_batch_kernel(const Args a, int byte_mode) {
   extern __shared__ __align__(16) uint8_t bz[];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t bi = blockIdx.x, b = a.first_block + bi;
-  const uint32_t RING = a.ring_bytes, RM = RING - 1, LM = kLzLR - 1;
+  const uint32_t RING = RC ? RC : a.ring_bytes, RM = RING - 1, LM = kLzLR - 1;
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(bz));
   const uint32_t lring = ring + RING, tab = ring + RING + kLzTab, flg = ring + RING + kLzFlg;
   const BlockEntry e = load_entry(a.src, b, lane);
@@ -1629,16 +1631,13 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     case GOMP_STRAT_DE: {
       const size_t smem = lzb_smem_bytes(a.ring_bytes);
       // a grid of at most one CTA per SM leaves the SMs latency-bound: the low-latency copies win there
-      if (stats) {
-        cudaFuncSetAttribute(lz77_batch_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        lz77_batch_kernel<true, false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
-      } else if (nblk <= sm_count() * kLowLatCtasPerSm) {
-        cudaFuncSetAttribute(lz77_batch_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        lz77_batch_kernel<false, true><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
-      } else {
-        cudaFuncSetAttribute(lz77_batch_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        lz77_batch_kernel<false, false><<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
-      }
+      constexpr uint32_t kRing0 = 16384;   // the default window's ring (compile-time masks and offsets)
+      const bool r0 = a.ring_bytes == kRing0, lowlat = nblk <= sm_count() * kLowLatCtasPerSm;
+      const auto kern = stats ? lz77_batch_kernel<true, false, 0>
+                        : lowlat ? (r0 ? lz77_batch_kernel<false, true, kRing0> : lz77_batch_kernel<false, true, 0>)
+                                 : (r0 ? lz77_batch_kernel<false, false, kRing0> : lz77_batch_kernel<false, false, 0>);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      kern<<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
       break;
     }
     case GOMP_STRAT_MRR: launch_lz77<GOMP_STRAT_MRR>(a, stats, byte_mode, st); break;
