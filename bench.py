@@ -66,7 +66,10 @@ def ncu_traffic(kernel, config):
         with open(path) as fh:
             t = json.load(fh)
         e = t[config][kernel]
-        return {"bytes": int(e["dram_read"] + e["dram_write"]), "source": e["source"]}
+        r = {"bytes": int(e["dram_read"] + e["dram_write"]), "source": e["source"]}
+        if "issue_active" in e:
+            r["issue"] = {"issue_active": e["issue_active"], "alu_pipe": e["alu_pipe"], "source": e["source"]}
+        return r
     except (OSError, KeyError, ValueError):
         return None
 
@@ -293,6 +296,7 @@ def main():
                 "frac": round(achieved / P, 4), "traffic": traffic["bytes"] if traffic else None,
                 "kernel": dom, "kernel_ms": round(kd_ms, 4), "algorithmic_bytes_per_launch": kbytes,
                 "traffic_source": traffic["source"] if traffic else None, "peak_source": peak_src,
+                "issue": traffic.get("issue") if traffic else None,
                 "kernels_ms": {k: round(v[0], 4) for k, v in kern.items()},
                 "step": {"algorithmic_bytes": U + C, "achieved": round((U + C) / (t_step * 1e-3) / 1e9, 2),
                          "frac": round((U + C) / (t_step * 1e-3) / 1e9 / P, 4)}}
