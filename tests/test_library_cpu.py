@@ -7,6 +7,7 @@ import subprocess
 
 import numpy as np
 import pytest
+import torch
 
 import datagen
 import oracle
@@ -156,3 +157,23 @@ def test_decoder_choice_follows_the_measured_crossover():
         info = gomp.get_info(c)
         avg = (info.file_len - info.payload_base) * 8 / info.n_sub_total
         assert gomp.huff_variant(info) == ("warp" if avg >= 8192 else "thread") == want, avg
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    """No CPU fallback: without libgompresso.so every entry point raises instead of computing on the host."""
+    monkeypatch.setattr(gomp, "LIB_PATH", str(tmp_path / "libgompresso.so"))
+    monkeypatch.setattr(gomp, "_lib", None)
+    x = np.frombuffer(b"abcabcabcabc" * 100, dtype=np.uint8)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        gomp.compress(x)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        gomp.get_info(np.zeros(64, dtype=np.uint8))
+
+
+def test_decompress_rejects_host_tensors():
+    """The decompression entry points take CUDA tensors only (no silent host path)."""
+    c = gomp.compress(np.frombuffer(b"hello hello hello" * 50, dtype=np.uint8))
+    info = gomp.get_info(c)
+    t = torch.zeros(16, dtype=torch.uint8)
+    with pytest.raises(ValueError, match="no CPU fallback"):
+        gomp.decompress_into(info, c, t, t)
