@@ -1,4 +1,4 @@
-"""Dev helper: LZ77 kernel time (unloaded 8 blocks / loaded 1024 blocks of C2) for libgompresso.so and exp/lzexp*.so."""
+"""Dev helper: LZ77 kernel time (unloaded 8 blocks / loaded 1024 blocks of C2) for libgompresso.so and every exp/*.so (argv[1]: comma-separated block counts)."""
 import sys, statistics, glob
 sys.path.insert(0, '.')
 import torch, bench, paper_1606_00519_b200 as gomp
