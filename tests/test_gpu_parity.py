@@ -103,6 +103,17 @@ def test_code_length_limits(cwl):
     _check(c, x, ["auto"])
 
 
+@pytest.mark.parametrize("cwl", [10, 15])
+@pytest.mark.parametrize("kind", ["wiki", "random"])
+def test_split_grid_decode(cwl, kind):
+    """A few blocks with 32 long sub-blocks each take the split speculative-decoder grid (two CTAs per block,
+    half of its sub-blocks each), with table-index and longer (canonical path) codes."""
+    x = (datagen.wiki if kind == "wiki" else datagen.random_bytes)(3 * 262144 - 4099, seed=31)
+    c = gomp.compress(x, mode="bit", cwl=cwl, block_size=262144, sub_block_seqs=0, sub_blocks_per_block=32)
+    assert gomp.huff_variant(gomp.get_info(c)) == "warp"
+    _check(c, x, ["auto"])
+
+
 @pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 65535, 65536, 65537, 3 * 65536 - 1])
 @pytest.mark.parametrize("mode", ["byte", "bit"])
 def test_sizes_and_ragged_tails(n, mode):
