@@ -1613,7 +1613,12 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     } else {
       // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block, rounds
       // of nt sub-blocks staged together
-      const uint32_t nt = uint32_t(std::min<uint64_t>(256, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
+      // with >= 6 blocks per SM, 128 threads: rounds of 128 sub-blocks wait for a slower sub-block less often
+      // than rounds of 256, and the smaller stage lets ~8 CTAs share an SM (C3 D=1 S=16, 1024 blocks: 0.93 vs
+      // 1.26 ms; 64/96/192 measured slower); fewer, larger blocks keep 256 threads per block (C5 1 MiB blocks:
+      // 128 threads lose 21%)
+      const uint32_t nt_max = nblk >= 6 * sm_count() ? 128u : 256u;
+      const uint32_t nt = uint32_t(std::min<uint64_t>(nt_max, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
       const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * nt * 3 / 2 + 512)));
       const size_t smem = tabs + cap;
       if (LONGc) {
