@@ -220,6 +220,20 @@ gomp_status gomp_decompress_stats(const void* d_workspace, void* stream, gomp_st
  */
 gomp_status gomp_plan_shards(const uint8_t* file, size_t len, int n_dev, uint32_t* first_block);
 
+/*
+ * Standalone shard file ("scatter compressed ranges plus the table slices"):
+ * write to out (HOST, capacity cap) a valid FORMAT.md file holding blocks [first_block, first_block + n_blocks)
+ * of file (HOST, len bytes; header + tables + those payloads must lie inside it). Its header carries the shard's
+ * block count, uncompressed length, sub-block count and max_block_tokens; block entries are rebased (payload
+ * offsets into the shard, sub_first into the shard's sub-table); payloads are copied in block order. Decoding it
+ * gives bytes [first_block * block_size, ...) of the whole file's output, so a device needs O(shard) memory.
+ * out = NULL: only *out_len (required size) is written. Blocks are independent: no data changes.
+ * Errors: INVALID_ARG (range, NULL out_len), TRUNCATED, header errors as gomp_get_info, HEADER_INCONSISTENT
+ * (an entry of the range points outside the file), DST_TOO_SMALL.
+ */
+gomp_status gomp_shard_file(const uint8_t* file, size_t len, uint32_t first_block, uint32_t n_blocks, uint8_t* out,
+                            size_t cap, size_t* out_len);
+
 #ifdef __cplusplus
 }
 #endif

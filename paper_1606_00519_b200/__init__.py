@@ -68,7 +68,7 @@ _lib = None
 EXPORTS = ["gomp_version", "gomp_status_string", "gomp_params_default", "gomp_compress_bound", "gomp_compress",
            "gomp_get_info", "gomp_validate_tables", "gomp_decompress_workspace_size", "gomp_decompress",
            "gomp_decompress_blocks", "gomp_decompress_host", "gomp_decompress_error", "gomp_decompress_stats",
-           "gomp_plan_shards", "gomp_compress_device_workspace_size", "gomp_compress_device"]
+           "gomp_plan_shards", "gomp_compress_device_workspace_size", "gomp_compress_device", "gomp_shard_file"]
 
 
 def lib():
@@ -100,6 +100,7 @@ def lib():
     L.gomp_decompress_error.argtypes = [vp, vp, ctypes.POINTER(Error)]
     L.gomp_decompress_stats.argtypes = [vp, vp, ctypes.POINTER(Stats)]
     L.gomp_plan_shards.argtypes = [u8p, sz, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+    L.gomp_shard_file.argtypes = [u8p, sz, u32, u32, u8p, sz, ctypes.POINTER(ctypes.c_size_t)]
     for f in EXPORTS[2:]:
         if f not in ("gomp_params_default", "gomp_compress_bound"):
             getattr(L, f).restype = ctypes.c_int
@@ -316,40 +317,46 @@ def plan_shards(c_host, n_dev):
     return list(first)
 
 
+def shard_file(c_host, first_block, n_blocks):
+    """gomp_shard_file: a standalone file (CPU torch.uint8 tensor) of blocks [first_block, first_block + n_blocks)
+    with rebased tables; it decodes to bytes [first_block * block_size, ...) of the whole output."""
+    f = _host_u8(c_host)
+    n = ctypes.c_size_t(0)
+    _check(lib().gomp_shard_file(f.ctypes.data, len(f), first_block, n_blocks, None, 0, ctypes.byref(n)),
+           "gomp_shard_file")
+    out = np.empty(n.value, dtype=np.uint8)
+    _check(lib().gomp_shard_file(f.ctypes.data, len(f), first_block, n_blocks, out.ctypes.data, n.value,
+                                 ctypes.byref(n)), "gomp_shard_file")
+    return torch.from_numpy(out)
+
+
 def decompress_sharded(c_host, devices, strategy="auto"):
     """Decompress one file across several GPUs of this process (blocks are independent,
     P:30-31): gomp_plan_shards splits the blocks into contiguous ranges balanced by compressed bytes; device d
-    receives the header and tables plus the payloads of its range (host->device from pinned memory on its own
-    stream) and decodes blocks [first[d], first[d+1]) with gomp_decompress_blocks. No collective, no gather:
+    receives only the shard file of its range (gomp_shard_file: rebased tables + its payloads, host->device from
+    pinned memory on its own stream), so its memory is O(shard), and decodes it. No collective, no gather:
     returns [(first_block, CUDA uint8 tensor of that range's output)] in device order."""
     f = _host_u8(c_host)
     info = get_info(f)
     devices = [torch.device(d) for d in devices]
     first = plan_shards(f, len(devices))
-    h = torch.from_numpy(f).pin_memory()
-    bt = f[64:64 + 32 * info.n_blocks].view(np.uint32).reshape(-1, 8) if info.n_blocks else np.zeros((0, 8), np.uint32)
     outs, pending = [], []
     for d, dev in enumerate(devices):
         b0, b1 = first[d], first[d + 1]
-        lo_out = min(b0 * info.block_size, info.uncompressed_len)
-        hi_out = min(b1 * info.block_size, info.uncompressed_len)
+        h = shard_file(f, b0, b1 - b0).pin_memory()
+        sinfo = get_info(h)
         with torch.cuda.device(dev):
             stream = torch.cuda.Stream(dev)
             with torch.cuda.stream(stream):   # allocations and copies ordered on this device's stream
-                src = torch.empty(info.file_len, dtype=torch.uint8, device=dev)
-                out = torch.empty(max(hi_out - lo_out, 1), dtype=torch.uint8, device=dev)
-                ws = torch.empty(workspace_size(info, max(b1 - b0, 1)), dtype=torch.uint8, device=dev)
-                src[: info.payload_base].copy_(h[: info.payload_base], non_blocking=True)
-                if b1 > b0:
-                    p0 = int(bt[b0, 0]) | (int(bt[b0, 1]) << 32)
-                    p1 = int(bt[b1 - 1, 0]) | (int(bt[b1 - 1, 1]) << 32)
-                    p1 = min(p1 + int(bt[b1 - 1, 2]) + 16, info.file_len)
-                    src[p0:p1].copy_(h[p0:p1], non_blocking=True)
-                    decompress_into(info, src, out, ws, strategy, stream, first_block=b0, n_blocks=b1 - b0)
-            pending.append((dev, stream, ws, src))   # src stays referenced until its stream is synchronised
-            outs.append((b0, out[: hi_out - lo_out]))
-    for dev, stream, ws, _ in pending:
+                src = torch.empty(h.numel(), dtype=torch.uint8, device=dev)
+                out = torch.empty(max(sinfo.uncompressed_len, 1), dtype=torch.uint8, device=dev)
+                ws = torch.empty(workspace_size(sinfo), dtype=torch.uint8, device=dev)
+                src.copy_(h, non_blocking=True)
+                decompress_into(sinfo, src, out, ws, strategy, stream)
+            pending.append((dev, stream, ws, b0, src, h))   # buffers stay referenced until the stream syncs
+            outs.append((b0, out[: sinfo.uncompressed_len]))
+    for dev, stream, ws, b0, _, _ in pending:
         e = read_error(ws, stream)
-        if e.status:
-            raise GompError(e.status, e.block, e.detail, where=f"decompress_sharded({dev})")
+        if e.status:   # the shard's block index, reported as the whole file's block index
+            raise GompError(e.status, b0 + e.block, e.detail, where=f"decompress_sharded({dev})")
     return outs

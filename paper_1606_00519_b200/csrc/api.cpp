@@ -111,3 +111,62 @@ GOMP_EXPORT gomp_status gomp_plan_shards(const uint8_t* f, size_t len, int n_dev
   first_block[n_dev] = in.n_blocks;
   return GOMP_OK;
 }
+
+// Standalone file of blocks [first, first + n): header with the shard's block count and length,
+// the block entries with payload offsets and sub-table indices rebased, the shard's sub-table entries, and the
+// payloads packed in block order (16-byte aligned), so a device holds O(shard) bytes instead of the whole file.
+GOMP_EXPORT gomp_status gomp_shard_file(const uint8_t* f, size_t len, uint32_t first, uint32_t n, uint8_t* out,
+                                        size_t cap, size_t* out_len) {
+  gomp_info in;
+  if (!out_len) return GOMP_ERR_INVALID_ARG;
+  gomp_status st = parse_header(f, len, &in);
+  if (st != GOMP_OK) return st;
+  if (uint64_t(first) + n > in.n_blocks) return GOMP_ERR_INVALID_ARG;
+  if (len < in.payload_base) return GOMP_ERR_TRUNCATED;
+  const bool bit = in.mode == GOMP_MODE_BIT;
+  uint64_t n_sub = 0, pay = 0, max_tok = 0;
+  for (uint32_t b = first; b < first + n; ++b) {
+    BlockEntry e;
+    std::memcpy(&e, f + kHeaderBytes + uint64_t(kBlockEntryBytes) * b, sizeof(e));
+    if (e.payload_off % 16 || e.payload_len % 16 || e.payload_off < in.payload_base ||
+        e.payload_off + e.payload_len > std::min<uint64_t>(len, in.file_len)) return GOMP_ERR_HEADER_INCONSISTENT;
+    if (bit && uint64_t(e.sub_first) + e.n_sub > in.n_sub_total) return GOMP_ERR_HEADER_INCONSISTENT;
+    n_sub += bit ? e.n_sub : 0;
+    pay += e.payload_len;
+    max_tok = std::max<uint64_t>(max_tok, 4ull * e.n_seq + e.n_lit);
+  }
+  const uint64_t total_lo = uint64_t(first) * in.block_size;
+  const uint64_t total = std::min<uint64_t>(uint64_t(first + n) * in.block_size, in.uncompressed_len) -
+                         std::min<uint64_t>(total_lo, in.uncompressed_len);
+  const uint64_t base = align16(kHeaderBytes + uint64_t(kBlockEntryBytes) * n + uint64_t(kSubEntryBytes) * n_sub);
+  const uint64_t flen = base + pay + kTrailerBytes;
+  *out_len = size_t(flen);
+  if (!out) return GOMP_OK;                 // size query
+  if (cap < flen) return GOMP_ERR_DST_TOO_SMALL;
+  std::memset(out, 0, size_t(base));
+  std::memcpy(out, f, kHeaderBytes);
+  st32(out + 20, n);
+  st64(out + 24, total);
+  st64(out + 32, flen);
+  st32(out + 40, uint32_t(n_sub));
+  st32(out + 44, bit ? uint32_t(max_tok) : 0u);
+  st64(out + 48, base);
+  uint64_t at = base, sub_at = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    BlockEntry e;
+    std::memcpy(&e, f + kHeaderBytes + uint64_t(kBlockEntryBytes) * (first + i), sizeof(e));
+    std::memcpy(out + at, f + e.payload_off, e.payload_len);
+    if (bit) {
+      std::memcpy(out + kHeaderBytes + uint64_t(kBlockEntryBytes) * n + uint64_t(kSubEntryBytes) * sub_at,
+                  f + kHeaderBytes + uint64_t(kBlockEntryBytes) * in.n_blocks + uint64_t(kSubEntryBytes) * e.sub_first,
+                  uint64_t(kSubEntryBytes) * e.n_sub);
+      e.sub_first = uint32_t(sub_at);
+      sub_at += e.n_sub;
+    }
+    e.payload_off = at;
+    std::memcpy(out + kHeaderBytes + uint64_t(kBlockEntryBytes) * i, &e, sizeof(e));
+    at += e.payload_len;
+  }
+  std::memset(out + at, 0, kTrailerBytes);
+  return GOMP_OK;
+}

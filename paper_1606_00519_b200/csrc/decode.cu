@@ -1060,7 +1060,9 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
   const uint8_t* base;
-  bool ok = e.n_lit <= ulen && e.n_seq <= ulen;
+  // Byte records may be empty (lit_len 0, no back-reference): the oracle's expansion accepts them, so n_seq is
+  // bounded by the payload only; Bit sequences are never empty (a literal or a length code closes each)
+  bool ok = e.n_lit <= ulen && (byte_mode || e.n_seq <= ulen);
   if (byte_mode) {
     ok = ok && payload_ok(a, e) && 4ull * e.n_seq + e.n_lit <= e.payload_len && e.S == 0 && e.n_sub == 0 && e.sub_first == 0;
     base = a.src + e.payload_off;
@@ -1106,7 +1108,7 @@ __global__ void __launch_bounds__(32 * kLz77Warps) lz77_kernel(const Args a, int
     const uint32_t op = o_carry + (ex >> 16);
     const uint32_t dst = op + lit;
     const uint32_t src = dst - dist;
-    const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst);
+    const bool bad_ref = act && L && (dist < L || dist > a.window || dist > dst || L > a.max_match);
     const bool bad_rec = act && !mcode && (r >> 16);
     const uint32_t lit_sum = tot & 0xffffu, out_sum = tot >> 16;
     const bool bad_sz = o_carry + out_sum > ulen || l_carry + lit_sum > e.n_lit;
@@ -1293,7 +1295,9 @@ __global__ void __launch_bounds__(32 * kBW, 8) lz77_batch_kernel(const Args a, i
   const BlockEntry e = load_entry(a.src, b, lane);
   const uint32_t ulen = block_ulen(a, b);
   const uint8_t* base;
-  bool ok = e.n_lit <= ulen && e.n_seq <= ulen;
+  // Byte records may be empty (lit_len 0, no back-reference): the oracle's expansion accepts them, so n_seq is
+  // bounded by the payload only; Bit sequences are never empty (a literal or a length code closes each)
+  bool ok = e.n_lit <= ulen && (byte_mode || e.n_seq <= ulen);
   if (byte_mode) {
     ok = ok && payload_ok(a, e) && 4ull * e.n_seq + e.n_lit <= e.payload_len && e.S == 0 && e.n_sub == 0 && e.sub_first == 0;
     base = a.src + e.payload_off;
@@ -1349,7 +1353,8 @@ __global__ void __launch_bounds__(32 * kBW, 8) lz77_batch_kernel(const Args a, i
     // 1 = malformed record (reported here), 2 = the group breaks the DE rule (its source neither precedes the
     // group nor lies in the sequence's own literals; R2/A4), 4 = a source may precede the block (exact test below)
     const bool has = act && L;
-    const bool lbad = act && (L ? (dist < L || dist > a.window) : (r >> 16) != 0);
+    // FORMAT.md §2: dist >= L (R2), dist <= window (R9), L <= max_match (a 6-bit mcode reaches min_match + 62)
+    const bool lbad = act && (L ? (dist < L || dist > a.window || L > a.max_match) : (r >> 16) != 0);
     const bool any_lbad = __any_sync(FULL, lbad);
     const bool de_ok = __all_sync(FULL, !has || dist >= (ex >> 16) + lit + L || dist <= lit);
     const bool maybe_neg = __any_sync(FULL, has && dist > oB + (ex >> 16) + lit);

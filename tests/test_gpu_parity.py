@@ -164,6 +164,11 @@ def _expect(status, f, strategy="auto"):
 def test_device_errors_byte():
     _expect("MALFORMED_BACKREF", byte_file([([(4, 4, 2)], b"abcd")], block_size=16))          # overlap (R2)
     _expect("MALFORMED_BACKREF", byte_file([([(2, 4, 5)], b"ab")], block_size=16))            # before block
+    f = byte_file([([(65, 65, 65)], b"a" * 65)], block_size=144, max_match=64)                # L > max_match
+    _expect("MALFORMED_BACKREF", f)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.decompress(f)
+    assert e.value.name == "MALFORMED_BACKREF"
     _expect("MALFORMED_BACKREF", byte_file([([(16, 0, 0)], b"a" * 16), ([(8, 4, 8), (0, 4, 12)], b"b" * 8)],
                                            block_size=16, window=8))                          # beyond window
     f = byte_file([([(3, 0, 0)], b"abc")], block_size=16)
@@ -177,62 +182,128 @@ def test_device_errors_byte():
     assert e.value.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT") and e.value.block == 2
 
 
-def test_device_errors_bit_fuzz():
-    """Bit flips in payloads are detected (or decode to wrong bytes) without crashing; tables are checked."""
+# Corrupted files: the GPU must raise iff the oracle raises (the definition: sequential expansion, P:767-779,
+# with the FORMAT.md §2 checks), and when both succeed the outputs must be identical byte for byte. Which status
+# wins may differ (the oracle stops at the first bad sequence of the first bad block, the device reports the
+# first error any CTA records), so only the class is compared: every device status is a format error.
+FORMAT_ERRORS = ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT")
+
+
+def _agree(f, strategies=("auto",)):
+    """Run f through the oracle and the GPU (each strategy); returns (oracle status or 'ok', gpu statuses)."""
+    try:
+        ref, o_st = oracle.decompress(f), "ok"
+    except oracle.OracleError as e:
+        ref, o_st = None, e.name
+    g_sts = []
+    for s in strategies:
+        try:
+            y, g_st = _gpu(f, s).cpu().numpy(), "ok"
+        except gomp.GompError as e:
+            y, g_st = None, e.name
+        assert (o_st == "ok") == (g_st == "ok"), f"strategy {s}: oracle {o_st}, gpu {g_st}"
+        if g_st == "ok":
+            assert np.array_equal(y, ref), f"strategy {s}: both accept, outputs differ"
+        else:
+            assert g_st in FORMAT_ERRORS, g_st
+        g_sts.append(g_st)
+    return o_st, g_sts
+
+
+def _flip(c, rng, lo, hi, n):
+    bad = c.copy()
+    for _ in range(n):
+        pos = int(rng.integers(lo, hi))
+        bad[pos] ^= np.uint8(1 << int(rng.integers(0, 8)))
+    return bad
+
+
+@pytest.mark.parametrize("sub", [("k", 8), ("S", 16)])
+def test_device_errors_bit_fuzz(sub):
+    """Bit flips in Bit payloads (trees, bitstreams), block-table and sub-table entries: GPU raises iff the
+    oracle does, identical output otherwise. k=8 sub-blocks of ~3 kbit per block go through the speculative
+    warp decoder, S=16 through the thread decoder."""
     import struct
     x = datagen.wiki(200_000, seed=2)
-    c = gomp.compress(x, mode="bit", block_size=32768, sub_block_seqs=0, sub_blocks_per_block=8).numpy()
+    kw = dict(sub_block_seqs=0, sub_blocks_per_block=sub[1]) if sub[0] == "k" else dict(sub_block_seqs=sub[1])
+    c = gomp.compress(x, mode="bit", block_size=32768, **kw).numpy()
+    info = gomp.get_info(c)
     off = struct.unpack_from("<Q", c.tobytes(), 64)[0]
     rng = np.random.default_rng(0)
-    for _ in range(30):
-        bad = c.copy()
-        pos = int(rng.integers(off, off + 3000))
-        bad[pos] ^= np.uint8(1 << int(rng.integers(0, 8)))
-        try:
-            y = _gpu(bad).cpu().numpy()
-            assert not np.array_equal(y, x) or pos < off + 160
-        except gomp.GompError as e:
-            assert e.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF"), e
+    seen = {}
+    regions = [(off, off + 3000), (off, len(c) - 16), (64, 64 + 32 * info.n_blocks), (64 + 32 * info.n_blocks, off)]
+    for i in range(80):
+        lo, hi = regions[i % len(regions)]
+        o_st, g = _agree(_flip(c, rng, lo, hi, int(rng.integers(1, 3))), ("auto", "mrr"))
+        seen[o_st] = seen.get(o_st, 0) + 1
+    assert seen.get("CORRUPT_STREAM", 0) > 0, seen
     bad = c.copy()
     bad[64 + 12] += 1  # n_seq of block 0
     with pytest.raises(gomp.GompError) as e:
         _gpu(bad)
     assert e.value.name in ("HEADER_INCONSISTENT", "CORRUPT_STREAM") and e.value.block == 0
+    with pytest.raises(oracle.OracleError):
+        oracle.decompress(bad)
     bad = c.copy()
     bad[64 + 28] += 1  # n_sub of block 0: no longer ceil(n_seq / S)
     with pytest.raises(gomp.GompError) as e:
         _gpu(bad)
     assert e.value.name == "HEADER_INCONSISTENT" and e.value.block == 0
+    with pytest.raises(oracle.OracleError):
+        oracle.decompress(bad)
+    assert np.array_equal(_gpu(c).cpu().numpy(), x)
 
 
 @pytest.mark.parametrize("de", [True, False])
 @pytest.mark.parametrize("n,bs", [(300_000, 16384), (2_200_000, 4096)])
 def test_device_errors_byte_fuzz(de, n, bs):
-    """Byte flips in Byte-format records and literals (the LZ77 kernels read them straight from the file): every
-    run ends with a reported format error or with some output, never a crash or a hang. 537 blocks of 4 KiB take
-    the throughput LZ77 copy variant, 19 blocks of 16 KiB the latency variant."""
+    """Byte flips in Byte-format records and literals (the LZ77 kernels read them straight from the file) and in
+    the block table: GPU raises iff the oracle does, for every strategy, identical output otherwise. 537 blocks of
+    4 KiB take the throughput LZ77 copy variant, 19 blocks of 16 KiB the latency variant."""
     import struct
     x = datagen.wiki(n, seed=21)
     c = gomp.compress(x, mode="byte", de=de, block_size=bs).numpy()
     nb = gomp.get_info(c).n_blocks
     off = struct.unpack_from("<Q", c.tobytes(), 64)[0]
     rng = np.random.default_rng(7)
-    seen = set()
-    for _ in range(40):
-        bad = c.copy()
-        for _ in range(int(rng.integers(1, 4))):
-            pos = int(rng.integers(off, len(c)))
-            bad[pos] ^= np.uint8(1 << int(rng.integers(0, 8)))
-        try:
-            y = _gpu(bad).cpu().numpy()
-            assert y.shape == x.shape
-            seen.add("ok" if np.array_equal(y, x) else "wrong")
-        except gomp.GompError as e:
-            assert e.name in ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT"), e
-            assert e.block < nb
-            seen.add(e.name)
-    assert seen & {"CORRUPT_STREAM", "MALFORMED_BACKREF"}   # record damage is detected
-    assert np.array_equal(_gpu(c).cpu().numpy(), x)           # and the device is still fine
+    seen = {}
+    for i in range(60):
+        lo, hi = (off, len(c) - 16) if i % 4 else (64, 64 + 32 * nb)
+        o_st, g = _agree(_flip(c, rng, lo, hi, int(rng.integers(1, 4))), ("auto", "de", "mrr", "sc"))
+        seen[o_st] = seen.get(o_st, 0) + 1
+    assert set(seen) & {"CORRUPT_STREAM", "MALFORMED_BACKREF"}, seen   # record damage is detected
+    assert np.array_equal(_gpu(c).cpu().numpy(), x)                      # and the device is still fine
+
+
+def test_device_errors_byte_record_fields():
+    """Every field of a Byte record pushed just past its FORMAT.md §2 limit, one at a time, in the first and in a
+    later warp group of a block: the oracle and the GPU (all strategies) both reject, and both accept the limit."""
+    seqs = [(5, 4, 5)] + [(1, 4, 5)] * 40
+    lits = bytes(range(65, 70)) + bytes(40)
+    good = [(seqs, lits)]
+    for blocks in (good, [([(256, 0, 0)], b"x" * 256)] + good):
+        f = byte_file(blocks, block_size=256)
+        assert _agree(f, ("auto", "de", "mrr", "sc"))[0] == "ok"
+    cases = {
+        "L > max_match (65 > 64)": ([(65, 0, 0), (0, 65, 65)], b"q" * 65, dict(max_match=64)),
+        "L > max_match, min_match 3": ([(70, 0, 0), (0, 64, 64)], b"q" * 70, dict(min_match=3, max_match=63)),
+        "dist < L (overlap, R2)": ([(4, 0, 0), (0, 5, 4)], b"abcd", {}),
+        "dist > window (R9)": ([(64, 0, 0), (0, 8, 33)], b"w" * 64, dict(window=32)),
+        "dist > dst (before the block)": ([(4, 0, 0), (0, 4, None)], b"abcd", {}),
+    }
+    for name, (sq, lt, kw) in cases.items():
+        for pad in (0, 40):       # first group, or a later group of the same block
+            # None: dist = dst + 1 (the source starts one byte before the block)
+            sq2 = [(a, b, d if d is not None else pad + 5) for a, b, d in sq]
+            s2 = [(1, 0, 0)] * pad + sq2
+            l2 = b"p" * pad + lt
+            total = sum(a + b for a, b, _ in s2)
+            f = byte_file([(s2, l2)], block_size=max(16, (total + 15) // 16 * 16), **kw)
+            o_st, g = _agree(f, ("auto", "de", "mrr", "sc"))
+            assert o_st == "MALFORMED_BACKREF" and set(g) == {"MALFORMED_BACKREF"}, (name, pad, o_st, g)
+    # empty records (lit_len 0, no back-reference) are valid sequences for the definition, also past ulen
+    f = byte_file([([(3, 0, 0)] + [(0, 0, 0)] * 40 + [(1, 4, 4)], b"abcd")], block_size=16)
+    assert _agree(f, ("auto", "de", "mrr", "sc"))[0] == "ok"
 
 
 def test_blocks_range_and_shards():

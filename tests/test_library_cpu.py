@@ -177,3 +177,29 @@ def test_decompress_rejects_host_tensors():
     t = torch.zeros(16, dtype=torch.uint8)
     with pytest.raises(ValueError, match="no CPU fallback"):
         gomp.decompress_into(info, c, t, t)
+
+
+@pytest.mark.parametrize("mode", ["byte", "bit"])
+@pytest.mark.parametrize("kind,n", [("wiki", 700_001), ("matrix", 300_000)])
+def test_shard_file_rebased(mode, kind, n):
+    """gomp_shard_file: a shard of blocks [b0, b1) is a valid standalone file (host table
+    validation) that the oracle decodes to bytes [b0 * block_size, ...) of the input; its size is O(shard)."""
+    x = datagen.GENERATORS[kind](n, seed=8)
+    kw = dict(mode=mode, de=True, block_size=32768)
+    if mode == "bit":
+        kw.update(sub_block_seqs=0, sub_blocks_per_block=8)
+    c = gomp.compress(x, **kw)
+    info = gomp.get_info(c)
+    for b0, b1 in [(0, info.n_blocks), (0, 1), (3, 7), (info.n_blocks - 2, info.n_blocks), (5, 5)]:
+        s = gomp.shard_file(c, b0, b1 - b0)
+        gomp.validate_tables(s)
+        si = gomp.get_info(s)
+        assert si.n_blocks == b1 - b0
+        y = oracle.decompress(s.numpy()) if b1 > b0 else np.zeros(0, np.uint8)
+        lo = b0 * info.block_size
+        assert np.array_equal(y, x[lo: lo + si.uncompressed_len])
+        assert len(y) == min(b1 * info.block_size, n) - min(lo, n)
+        if b1 - b0 == 1:
+            assert si.file_len < info.file_len / 4
+    with pytest.raises(gomp.GompError):
+        gomp.shard_file(c, info.n_blocks - 1, 2)
