@@ -3,7 +3,7 @@ import glob, statistics, sys, time
 sys.path.insert(0, '.')
 import torch, bench, paper_1606_00519_b200 as gomp
 DEV = torch.device("cuda:0")
-kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+kind, n, seed, ckw = bench.CONFIGS["C2"][:4]
 x = bench.gen(kind, n, seed)
 c = gomp.compress(x, **ckw).pin_memory()
 info = gomp.get_info(c)

@@ -2,7 +2,7 @@
 import sys, statistics, glob
 sys.path.insert(0, '.')
 import torch, bench, paper_1606_00519_b200 as gomp
-kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+kind, n, seed, ckw = bench.CONFIGS["C2"][:4]
 x = bench.gen(kind, n, seed)
 c = gomp.compress(x, **ckw)
 for path in [gomp.LIB_PATH] + sorted(glob.glob("exp/*.so")):
