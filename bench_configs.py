@@ -5,7 +5,7 @@
 
 One JSON line per measured point, same timing rules as bench.py (CUDA events on the launching stream, W >= 3
 untimed warm-up steps, the 126 MB L2 flushed by a 512 MiB write between timed steps, device-resident inputs),
-every point checked against its input byte for byte before it is timed. value = uncompressed bytes / mean step
+every point checked against its input byte for byte before it is timed. value = uncompressed bytes / median step
 time (GB/s, 1e9); roofline_frac = (compressed + uncompressed bytes) / step time / HBM peak.
 
   C1  1 MiB English-like text, Byte, 64 KiB blocks, DE: single-launch latency and steady state (CUDA graph of
@@ -14,8 +14,8 @@ time (GB/s, 1e9); roofline_frac = (compressed + uncompressed bytes) / step time 
       file, with the MRR rounds histogram measured on the GPU (GOMP_FLAG_STATS run, untimed).
   C4  16 GiB Wikipedia-shaped corpus on one B200 = the C2 file's blocks tiled 64x (blocks are
       independent and the window is 8 KiB, so tiling keeps per-block statistics).
-  C5  MatrixMarket-shaped numeric text, Bit, DE: block size x sub-blocks-per-block sweep (256 MiB per point on
-      one GPU; BASELINE names 4 GiB on 8 GPUs, i.e. 512 MiB per GPU).
+  C5  4 GiB MatrixMarket-shaped numeric text (a 256 MiB file's blocks tiled 16x), Bit, DE: block size x
+      sub-blocks-per-block sweep on one GPU (BASELINE names 8 GPUs: 1/8 of the blocks each, no exchange).
   f2  the GPU compressor (gomp_compress_device) beside the host compressor, identical files required.
   f4  the paper's host-link modes at C2: "In/Out" and "In" through gomp_decompress_host.
 """
@@ -66,7 +66,7 @@ def point(tag, c, x_check, steps, strategy="auto", extra=None, stats=False):
     e = gomp.read_error(ws)
     ok = e.status == 0 and bool(x_check(out))
     ms = timed(lambda: gomp.decompress_into(info, d, out, ws, strategy), steps, 3)
-    t = statistics.mean(ms)
+    t = statistics.median(ms)
     P, _ = bench.peaks()
     line = {"config": tag, "value": round(U / (t * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(t, 4),
             "uncompressed_bytes": U, "compressed_bytes": C, "ratio": round(U / C, 4), "strategy": strategy,
@@ -75,8 +75,8 @@ def point(tag, c, x_check, steps, strategy="auto", extra=None, stats=False):
             "roofline_frac": round((U + C) / (t * 1e-3) / 1e9 / P, 4), "peak_gbs": P, "steps": steps,
             "parity": ok}
     if info.mode == 1:
-        kd = statistics.mean(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="decode"), 5, 3))
-        kl = statistics.mean(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="lz77"), 5, 3))
+        kd = statistics.median(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="decode"), 5, 3))
+        kl = statistics.median(timed(lambda: gomp.decompress_into(info, d, out, ws, strategy, phase="lz77"), 5, 3))
         line["kernels_ms"] = {"huff_" + gomp.huff_variant(info): round(kd, 4), "lz77": round(kl, 4)}
     if stats:
         gomp.decompress_into(info, d, out, ws, strategy, stats=True)
@@ -162,40 +162,14 @@ def run_c3(steps):
 
 
 def tile_file(c, times):
-    """A valid file whose blocks are the blocks of c repeated `times` times (c's last block must be full)."""
+    """A valid file whose blocks are the blocks of c repeated `times` times (c's last block must be full): bench.py's
+    tiled shard of the whole tiled range."""
     a = c.numpy()
-    info = gomp.get_info(a)
-    nb, ns, U = info.n_blocks, info.n_sub_total, info.uncompressed_len
-    assert U == nb * info.block_size, "tiling needs full blocks"
-    bt = a[64:64 + 32 * nb].copy().view(np.uint32).reshape(nb, 8)
-    st = a[64 + 32 * nb:64 + 32 * nb + 8 * ns]
-    pb, pend = info.payload_base, info.file_len - 16
-    pay = a[pb:pend]
-    base = -(-(64 + 32 * nb * times + 8 * ns * times) // 16) * 16
-    total = base + len(pay) * times + 16
-    f = np.zeros(total, dtype=np.uint8)
-    f[:64] = a[:64]
-    hv = f[:64].view(np.uint32)
-    hv[5] = nb * times
-    f[24:32] = np.frombuffer(np.uint64(U * times).tobytes(), np.uint8)
-    f[32:40] = np.frombuffer(np.uint64(total).tobytes(), np.uint8)
-    hv[10] = ns * times
-    f[48:56] = np.frombuffer(np.uint64(base).tobytes(), np.uint8)
-    bts = np.tile(bt, (times, 1))
-    off = bt[:, 0].astype(np.uint64) | (bt[:, 1].astype(np.uint64) << np.uint64(32))
-    for r in range(times):
-        o = off - np.uint64(pb) + np.uint64(base + r * len(pay))
-        bts[r * nb:(r + 1) * nb, 0] = (o & np.uint64(0xffffffff)).astype(np.uint32)
-        bts[r * nb:(r + 1) * nb, 1] = (o >> np.uint64(32)).astype(np.uint32)
-        bts[r * nb:(r + 1) * nb, 5] = bt[:, 5] + np.uint32(r * ns)
-    f[64:64 + 32 * nb * times] = bts.reshape(-1).view(np.uint8)
-    f[64 + 32 * nb * times:64 + 32 * nb * times + 8 * ns * times] = np.tile(st, times)
-    f[base:base + len(pay) * times] = np.tile(pay, times)
-    return torch.from_numpy(f)
+    return torch.from_numpy(bench.tiled_shard(a, 0, gomp.get_info(a).n_blocks * times))
 
 
 def run_c4(steps):
-    kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+    kind, n, seed, ckw = bench.CONFIGS["C2"][:4]
     x = bench.gen(kind, n, seed)
     c = tile_file(gomp.compress(x, **ckw), 64)
     xd = torch.from_numpy(x).to(DEV)
@@ -209,16 +183,26 @@ def run_c4(steps):
 
 
 def run_c5(steps):
+    """C5 at its BASELINE size: 4 GiB of MatrixMarket-shaped text = a 256 MiB matrix file's blocks tiled 16x (blocks
+    are independent, so tiling keeps every block's statistics), every block size x sub-block point on one B200
+    (BASELINE names 8 GPUs: each would hold 1/8 of the blocks, no exchange)."""
+    tiles = 16
     x = datagen.matrix(256 << 20, seed=5)
     xd = torch.from_numpy(x).to(DEV)
+    n = len(x)
+
+    def check(o):
+        return all(torch.equal(o[i * n:(i + 1) * n], xd) for i in range(tiles))
+
     for bs in (65536, 131072, 262144, 524288, 1 << 20):
         for sub in (4, 8, 16, 32, 64, "S16"):
             kw = dict(mode="bit", de=True, block_size=bs)
             kw.update(dict(sub_block_seqs=16) if sub == "S16" else dict(sub_blocks_per_block=sub))
-            c = gomp.compress(x, **kw)
-            point(f"C5-bs{bs // 1024}k-{'S16' if sub == 'S16' else f'k{sub}'}", c, lambda o: torch.equal(o, xd),
-                  steps, extra={"workload": "256 MiB MatrixMarket-shaped numeric text, Gompresso/Bit, DE",
-                                "sub_blocks": sub})
+            c = tile_file(gomp.compress(x, **kw), tiles)
+            point(f"C5-4GiB-bs{bs // 1024}k-{'S16' if sub == 'S16' else f'k{sub}'}", c, check, max(3, steps // 2),
+                  extra={"workload": "4 GiB MatrixMarket-shaped numeric text (256 MiB file tiled 16x), "
+                                     "Gompresso/Bit, DE, 1 B200", "sub_blocks": sub})
+            del c
 
 
 def run_f2(steps):
@@ -258,7 +242,7 @@ def run_f4(steps):
     """Host-link modes of the paper at C2: "In/Out" (compressed file in, output out: the bench's e2e)
     and "In" (compressed file in, output stays on the device), both through gomp_decompress_host with pinned
     buffers; the copy engines' own ceiling measured beside them."""
-    kind, n, seed, ckw, _ = bench.CONFIGS["C2"]
+    kind, n, seed, ckw = bench.CONFIGS["C2"][:4]
     x = bench.gen(kind, n, seed)
     c = gomp.compress(x, **ckw).pin_memory()
     info = gomp.get_info(c)

@@ -6,8 +6,10 @@
  * Conventions for every entry point
  *  - Plain pointers and sizes only. "host" pointers are CPU memory, "device" pointers are CUDA global memory
  *    of the device current on the calling thread; `stream` is a cudaStream_t (NULL = legacy default stream).
- *  - The caller owns every buffer. The library never allocates device memory and keeps no global mutable
- *    state; all functions are reentrant and safe for concurrent calls on different streams/devices.
+ *  - The caller owns every buffer. The library never allocates device memory. Its only state is a cache of
+ *    per-device launch facts (SM count, kernel shared-memory opt-ins, occupancies; mutex-guarded) and, for
+ *    gomp_decompress_host, one set of internal streams/events per host thread and device, created on first use
+ *    and reused; all functions are reentrant and safe for concurrent calls on different streams/devices.
  *  - Every function returns a gomp_status. Argument and host-header errors are returned synchronously;
  *    errors found by device kernels are recorded first-error-wins in the workspace and read with
  *    gomp_decompress_error() after the stream work completes. On any error the output contents are

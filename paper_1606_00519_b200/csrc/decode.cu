@@ -16,8 +16,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <vector>
 #include <cstdint>
+#include <memory>
+#include <mutex>
+#include <vector>
 
 #include "format.hpp"
 #include "gomp.h"
@@ -1493,15 +1495,74 @@ __global__ void __launch_bounds__(32 * kBW, 8) lz77_batch_kernel(const Args a, i
 }
 
 
+// Launch facts cached per device: the SM count, the dynamic shared memory each kernel has been opted in to, and
+// the occupancy of (kernel, threads, shared memory) triples. After its first use on a device a decompression
+// call issues no attribute or occupancy query (C1's single-launch latency). One mutex guards the cache: the
+// library's entry points may be called from several host threads, on several devices.
+constexpr int kMaxDevices = 64;
+struct LaunchCache {
+  std::mutex mu;
+  int sms[kMaxDevices] = {};
+  struct Attr { int dev; const void* f; size_t smem; };
+  struct Occ { int dev; const void* f; int threads; size_t smem; int occ; };
+  std::vector<Attr> attrs;
+  std::vector<Occ> occs;
+};
+LaunchCache& launch_cache() {
+  static LaunchCache c;
+  return c;
+}
+int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess && d >= 0 && d < kMaxDevices ? d : 0;
+}
+uint32_t sm_count() {
+  const int dev = current_device();
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  if (!c.sms[dev]) {
+    int v = 0;
+    c.sms[dev] = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0 ? v : 1;
+  }
+  return uint32_t(c.sms[dev]);
+}
+// opt kernel f in to `smem` bytes of dynamic shared memory on the current device (once per larger size)
+template <class F>
+void ensure_smem(F* f, size_t smem) {
+  const int dev = current_device();
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (auto& a : c.attrs)
+    if (a.dev == dev && a.f == reinterpret_cast<const void*>(f)) {
+      if (a.smem < smem && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) == cudaSuccess)
+        a.smem = smem;
+      return;
+    }
+  if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) == cudaSuccess)
+    c.attrs.push_back({dev, reinterpret_cast<const void*>(f), smem});
+}
+template <class F>
+int occupancy(F* f, int threads, size_t smem) {
+  const int dev = current_device();
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (const auto& o : c.occs)
+    if (o.dev == dev && o.f == reinterpret_cast<const void*>(f) && o.threads == threads && o.smem == smem) return o.occ;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, threads, smem) != cudaSuccess) occ = 0;
+  if (c.occs.size() < 256) c.occs.push_back({dev, reinterpret_cast<const void*>(f), threads, smem, occ});
+  return occ;
+}
+
 template <int S>
 void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
   const dim3 grid((a.n_blocks + kLz77Warps - 1) / kLz77Warps), block(32 * kLz77Warps);
   const size_t smem = lz77_smem_bytes(a.ring_bytes);
   if (stats) {
-    cudaFuncSetAttribute(lz77_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(lz77_kernel<S, true>, smem);
     lz77_kernel<S, true><<<grid, block, smem, st>>>(a, byte_mode ? 1 : 0);
   } else {
-    cudaFuncSetAttribute(lz77_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_smem(lz77_kernel<S, false>, smem);
     lz77_kernel<S, false><<<grid, block, smem, st>>>(a, byte_mode ? 1 : 0);
   }
 }
@@ -1509,15 +1570,6 @@ void launch_lz77(const Args& a, bool stats, bool byte_mode, cudaStream_t st) {
 
 // reset_ws: clear the error word / statistics first (a pipelined caller clears them once); tok_block0: block
 // slot of the workspace token buffer used for block `first` (pipelined chunks in flight use disjoint slots)
-// SMs of the current device (cached per process; one device type per node)
-uint32_t sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0, v = 0;
-    n = cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0 ? v : 1;
-  }
-  return uint32_t(n);
-}
 
 gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nblk, const uint8_t* d_src,
                              size_t src_len, uint8_t* d_dst, size_t dst_cap, void* d_ws, size_t ws_bytes,
@@ -1600,13 +1652,12 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / kHuffG, fit, avg_sub})));
       const size_t smem = tabs + ngr * slot;
       const auto kern = LONGc ? huff_warp_kernel<true, kHuffG> : huff_warp_kernel<false, kHuffG>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ensure_smem(kern, smem);
       // split grid: blocks that fill at most half of the resident CTA slots are each decoded by two CTAs taking
       // half of its sub-blocks (the idle slots would otherwise wait out whole-block latencies; measured on the
       // first 74 blocks of C2: 0.095 vs 0.149 ms). Splitting only the last partial wave of a large grid was
       // measured as no gain (C2: 0.674 vs 0.675 ms).
-      int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, int(32 * kHuffG * ngr), smem) != cudaSuccess) occ = 0;
+      const int occ = occupancy(kern, int(32 * kHuffG * ngr), smem);
       const uint32_t slots = uint32_t(std::max(occ, 0)) * sm_count();
       uint32_t grid = nblk;
       if (2 * uint64_t(nblk) <= slots && avg_sub >= 2 * uint64_t(ngr)) {
@@ -1627,10 +1678,10 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * nt * 3 / 2 + 512)));
       const size_t smem = tabs + cap;
       if (LONGc) {
-        cudaFuncSetAttribute(huff_thread_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        ensure_smem(huff_thread_kernel<true>, smem);
         huff_thread_kernel<true><<<nblk, nt, smem, st>>>(a, cap);
       } else {
-        cudaFuncSetAttribute(huff_thread_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        ensure_smem(huff_thread_kernel<false>, smem);
         huff_thread_kernel<false><<<nblk, nt, smem, st>>>(a, cap);
       }
     }
@@ -1646,7 +1697,7 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       const auto kern = stats ? lz77_batch_kernel<true, false, 0>
                         : lowlat ? (r0 ? lz77_batch_kernel<false, true, kRing0> : lz77_batch_kernel<false, true, 0>)
                                  : (r0 ? lz77_batch_kernel<false, false, kRing0> : lz77_batch_kernel<false, false, 0>);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      ensure_smem(kern, smem);
       kern<<<nblk, 32 * kBW, smem, st>>>(a, byte_mode ? 1 : 0);
       break;
     }
@@ -1677,30 +1728,43 @@ GOMP_EXPORT gomp_status gomp_decompress_blocks(const gomp_info* info, uint32_t f
 
 namespace gomp {
 namespace {
-// RAII set of the streams/events of one pipelined host call (destroyed once enqueued work no longer needs
-// them: CUDA releases a destroyed stream/event after its pending work completes)
+// Streams and events of the pipelined host path, created once per host thread and device and reused by every
+// call (C1 latency: creating 6 streams and up to 26 events per call cost tens of microseconds). A call records
+// its events in order; an event re-recorded by a later call has already been waited on (cudaStreamWaitEvent
+// captures the event's state when it is called).
 struct Pipe {
   cudaStream_t h2d = nullptr, d2h = nullptr, comp[kPipeStreams] = {};
   cudaEvent_t ev[2 * kPipeMaxChunks + 2] = {};
-  int nev = 0;
+  int nev = 0, made = 0;
   bool ok = true;
   Pipe() {
     ok = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) == cudaSuccess &&
          cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) == cudaSuccess;
     for (auto& c : comp) ok = ok && cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking) == cudaSuccess;
   }
+  void begin() { nev = 0; }
   cudaEvent_t event() {
     if (nev == int(sizeof(ev) / sizeof(ev[0]))) { ok = false; return nullptr; }
-    if (cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming) != cudaSuccess) { ok = false; return nullptr; }
+    if (nev == made) {
+      if (cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming) != cudaSuccess) { ok = false; return nullptr; }
+      ++made;
+    }
     return ev[nev++];
   }
-  ~Pipe() {
-    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+  ~Pipe() {   // at thread exit; errors (e.g. the context already torn down at process exit) are ignored
+    for (int i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
     for (auto& c : comp) if (c) cudaStreamDestroy(c);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
   }
 };
+Pipe* thread_pipe() {
+  thread_local std::unique_ptr<Pipe> pipes[kMaxDevices];
+  std::unique_ptr<Pipe>& p = pipes[current_device()];
+  if (!p || !p->ok) p.reset(new Pipe());
+  p->begin();
+  return p->ok ? p.get() : nullptr;
+}
 }  // namespace
 }  // namespace gomp
 
@@ -1747,8 +1811,9 @@ GOMP_EXPORT gomp_status gomp_decompress_host(const gomp_info* info, const uint8_
     if (!ordered) cb = {0, nb};
   }
   const uint32_t K = uint32_t(cb.size() - 1);
-  Pipe p;
-  if (!p.ok) return GOMP_ERR_CUDA;
+  Pipe* pp = thread_pipe();
+  if (!pp) return GOMP_ERR_CUDA;
+  Pipe& p = *pp;
   if (cudaMemsetAsync(d_ws, 0, kWsHeaderBytes, st) != cudaSuccess) return GOMP_ERR_CUDA;
   cudaEvent_t e0 = p.event();
   if (!p.ok || cudaEventRecord(e0, st) != cudaSuccess) return GOMP_ERR_CUDA;

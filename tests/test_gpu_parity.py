@@ -497,3 +497,56 @@ def test_decompress_sharded_reports_device_errors():
     c[off: off + 64] = 0xff                           # records with impossible back-references
     with pytest.raises(gomp.GompError):
         gomp.decompress_sharded(c, [DEV, DEV])
+
+
+def _edge_source_block(rng, block_size, window=8192):
+    """Sequences of one DE block whose back-reference sources end 0-3 bytes before their group's start: the word
+    loads of the OR-assembled copies then also read bytes of the current group, which other lanes
+    and warps are writing at that moment. Literal bytes are random, so a leaked neighbour byte shows."""
+    seqs, lits, o = [], bytearray(), 0
+    while True:
+        og = o
+        group = []
+        for _ in range(32):
+            lit = int(rng.integers(0, 7))
+            L = int(rng.integers(4, 13))
+            e = og - int(rng.integers(0, 4))                  # source end: at or just before the group start
+            dst = o + lit
+            if e - L < 0 or dst - (e - L) > window or o + lit + L > block_size - 64:
+                L, d = 0, 0
+            else:
+                d = dst - (e - L)
+            group.append((lit, L, d))
+            lits += bytes(rng.integers(0, 256, lit, dtype=np.uint8))
+            o += lit + L
+        seqs += group
+        if o > block_size - 1100:
+            break
+    while o < block_size:                                     # fill the block with literal-only sequences
+        lit = min(1023, block_size - o)
+        seqs.append((lit, 0, 0))
+        lits += bytes(rng.integers(0, 256, lit, dtype=np.uint8))
+        o += lit
+    return seqs, bytes(lits)
+
+
+@pytest.mark.parametrize("nblocks,bs", [(3, 16384), (40, 4096), (2, 65536)])
+def test_or_copy_overread_bytes_discarded(nblocks, bs):
+    """Directed test for the racecheck hazards of DESIGN.md §5: the OR-assembled word copies read up to 3 bytes on
+    either side of a source range (the funnel-shift neighbours) and those bytes may be written concurrently by
+    another lane or warp; they must never reach the output. Every source here ends 0-3 bytes before its group's
+    start, so the over-read bytes are exactly the ones being written; run repeatedly, every strategy and copy
+    variant (40 blocks of 4 KiB: throughput copies; 2-3 blocks: the latency copies) must equal the sequential
+    expansion byte for byte."""
+    from fmt_util import expand
+    rng = np.random.default_rng(bs + nblocks)
+    blocks = [_edge_source_block(rng, bs) for _ in range(nblocks)]
+    f = byte_file(blocks, block_size=bs, de=True)
+    want = b"".join(expand(s, l) for s, l in blocks)
+    ref = oracle.decompress(f)
+    assert bytes(ref) == want
+    assert oracle.verify_de(f)
+    for s in ("de", "mrr", "sc"):
+        for _ in range(5):
+            y = _gpu(f, s).cpu().numpy()
+            assert y.tobytes() == want, s
