@@ -141,8 +141,8 @@ gomp_status gomp_compress(const uint8_t* src, size_t src_len, uint8_t* dst, size
  * GPU compressor ("each block is LZ77-compressed by a group of threads"): the same
  * file as gomp_compress for the same input and parameters, byte for byte, computed on the device current on
  * the calling thread: one warp per block runs the greedy longest-match parse with DE (hash chains in shared
- * memory, 32 candidates compared per warp step), Byte payloads or Huffman coding (frequencies, canonical
- * codes and bit packing on the device; the package-merge code lengths on the host, as gomp_compress).
+ * memory, 32 candidates compared per warp step), Byte payloads or Huffman coding (frequencies, package-merge
+ * code lengths with the host routine's tie order, canonical codes and bit packing, all on the device).
  *   d_src      DEVICE input, src_len bytes (any alignment)
  *   d_dst      DEVICE output, 16-byte aligned, capacity dst_cap >= gomp_compress_bound(src_len, p)
  *   dst_len    HOST, receives the file size

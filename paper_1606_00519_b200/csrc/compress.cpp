@@ -309,7 +309,6 @@ uint64_t block_bound(const gomp_params* p) {
 // header layout as the host compressor, so both produce identical files
 bool host_params_ok(const gomp_params* p) { return params_ok(p); }
 uint64_t host_max_seqs(uint32_t bs, uint32_t mm) { return max_seqs(bs, mm); }
-void host_package_merge(const uint64_t* freq, int n, int maxlen, uint8_t* lens) { package_merge(freq, n, maxlen, lens); }
 void host_write_header(uint8_t* h, const gomp_params* p, uint32_t nb, uint64_t src_len, uint64_t file_len,
                        uint64_t n_sub_total, uint64_t max_tok, uint64_t base) {
   std::memcpy(h, "GMPR", 4);

@@ -12,7 +12,8 @@
 //                       (ties: smallest distance). Output: Byte-format records per block.
 //   byte_payload_kernel Gompresso/Byte payloads: records + the literal strings gathered from the input.
 //   freq_kernel         Gompresso/Bit: per-block literal/length and distance symbol counts (RFC 1951 alphabet, R15).
-//   (host)              package-merge code lengths <= CWL per block (R14), shared with the host compressor.
+//   pm_kernel           package-merge code lengths <= CWL per block (R14; the host compressor's algorithm and tie
+//                       order, so the files stay identical) and the sub-block size S (R12), on the device.
 //   huff_encode_kernel  canonical codes, per-sequence bit counts, a block-wide scan of bit offsets,
 //                       then every thread writes its sequence's bits (LSB-first, R15) at its offset: interior
 //                       32-bit words by plain stores, the two boundary words by atomicOr; sub-block bit sizes
@@ -23,7 +24,6 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
-#include <thread>
 #include <vector>
 
 #include "compress.hpp"
@@ -281,6 +281,106 @@ __global__ void __launch_bounds__(kCompThreads) freq_kernel(const CArgs a, uint3
   for (uint32_t s = threadIdx.x; s < 316; s += kCompThreads) freq[316ull * b + s] = fl[s];
 }
 
+// Package-merge code lengths <= cwl (R14) on the device, per block: warp 0 the 286 literal/length symbols, warp 1
+// the 30 distance symbols. The same algorithm and tie order as the host routine (compress.cpp package_merge):
+// leaves are the used symbols ordered by (frequency, symbol) (a warp rank sort), lists[cwl] = the leaves,
+// lists[d] = merge(leaves, pairs of lists[d+1]) with a leaf before a package of equal weight; the first 2m - 2
+// items of lists[1] are selected, a selected package selects the first 2P items of the next list, and a symbol's
+// length is the number of times it is selected. Lane 0 runs the merge (at most 2m - 1 items per list, 15 lists);
+// lane 0 of warp 2 derives the block's sub-block size S (R12). No host round trip between freq and encode.
+template <uint32_t N>   // alphabet size; a list holds at most 2N - 1 items
+struct PmSmem {
+  uint64_t w[2][2 * N];                // item weights of the previous and the current list
+  int16_t item[16][2 * N];             // item kinds per list: symbol (leaf) or -1 (package)
+  uint16_t cnt[16];                    // items per list
+  uint16_t sorted[N];
+  uint32_t f[N];
+};
+template <uint32_t N>
+__device__ void pm_table(PmSmem<N>& sm, const uint32_t* fr, uint32_t n, uint32_t maxlen, uint8_t* lens, uint32_t lane) {
+  // used symbols ranked by (frequency, symbol)
+  for (uint32_t i = lane; i < n; i += 32) sm.f[i] = fr[i];
+  __syncwarp();
+  uint32_t m = 0;
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint32_t fi = sm.f[i];
+    if (fi) {
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < n; ++j) {
+        const uint32_t fj = sm.f[j];
+        r += fj && (fj < fi || (fj == fi && j < i));
+      }
+      sm.sorted[r] = uint16_t(i);
+    }
+    m += fi != 0;
+  }
+  for (int d = 16; d; d >>= 1) m += __shfl_xor_sync(FULLM, m, d);
+  for (uint32_t i = lane; i < n; i += 32) lens[i] = 0;
+  __syncwarp();
+  if (lane != 0 || m == 0) return;
+  if (m == 1) { lens[sm.sorted[0]] = 1; return; }
+  uint32_t cur = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    sm.w[cur][i] = sm.f[sm.sorted[i]];
+    sm.item[maxlen][i] = int16_t(sm.sorted[i]);
+  }
+  sm.cnt[maxlen] = uint16_t(m);
+  for (uint32_t d = maxlen - 1; d >= 1; --d) {
+    const uint32_t np = sm.cnt[d + 1] / 2, nx = cur ^ 1u;
+    uint32_t a = 0, b = 0, k = 0;
+    while (a < m || b < np) {
+      const uint64_t pw = b < np ? sm.w[cur][2 * b] + sm.w[cur][2 * b + 1] : 0ull;
+      const uint64_t lw = a < m ? uint64_t(sm.f[sm.sorted[a]]) : 0ull;
+      if (b >= np || (a < m && lw <= pw)) {
+        sm.w[nx][k] = lw;
+        sm.item[d][k] = int16_t(sm.sorted[a]);
+        ++a;
+      } else {
+        sm.w[nx][k] = pw;
+        sm.item[d][k] = -1;
+        ++b;
+      }
+      ++k;
+    }
+    sm.cnt[d] = uint16_t(k);
+    cur = nx;
+  }
+  uint32_t take = 2 * m - 2;
+  for (uint32_t d = 1; d <= maxlen && take; ++d) {
+    uint32_t npk = 0;
+    for (uint32_t i = 0; i < take && i < sm.cnt[d]; ++i) {
+      const int s = sm.item[d][i];
+      if (s >= 0) ++lens[s];
+      else ++npk;
+    }
+    take = 2 * npk;
+  }
+}
+
+__global__ void __launch_bounds__(96) pm_kernel(const CArgs a, const uint32_t* freq, uint8_t* lens_out, uint32_t* Sb,
+                                                uint32_t cwl, uint32_t sub_block_seqs, uint32_t sub_blocks_per_block) {
+  __shared__ PmSmem<286> sml;
+  __shared__ PmSmem<30> smd;
+  __shared__ uint8_t lens[316];
+  const uint32_t b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t* fr = freq + 316ull * b;
+  if (w == 0) pm_table(sml, fr, 286, cwl, lens, lane);
+  else if (w == 1) pm_table(smd, fr + 286, 30, cwl, lens + 286, lane);
+  else if (lane == 0) {
+    const uint32_t ns = a.meta[4 * b];
+    uint32_t S = sub_block_seqs ? sub_block_seqs : (ns + sub_blocks_per_block - 1) / sub_blocks_per_block;
+    Sb[b] = S ? S : 1u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {   // R14: a block without back-references gets one dummy distance code
+    bool any = false;
+    for (int i = 0; i < 30; ++i) any |= lens[286 + i] != 0;
+    if (!any) lens[286] = 1;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 316; i += blockDim.x) lens_out[316ull * b + i] = lens[i];
+}
+
 // ------------------------------------------------------------------ Bit: encode one block
 // Writes the bits of one sequence, range [b0, b1) of the block stream, LSB-first: pending bits accumulate in a
 // 64-bit register; a 32-bit word is emitted once its last bit is pending: a plain store when the word lies wholly
@@ -499,53 +599,28 @@ GOMP_EXPORT gomp_status gomp_compress_device(const uint8_t* d_src, size_t src_le
   if (p->mode == GOMP_MODE_BIT && nb) {
     uint32_t* d_freq = reinterpret_cast<uint32_t*>(ws + Lw.freq_off);
     freq_kernel<<<nb, kCompThreads, 0, st>>>(a, d_freq);
-    std::vector<uint32_t> freq(316ull * nb);
-    if (cudaMemcpyAsync(freq.data(), d_freq, 4 * freq.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(meta.data(), a.meta, 16ull * nb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-      return GOMP_ERR_CUDA;
-    // package-merge code lengths per block on the host (the same routine as gomp_compress, R14)
-    std::vector<uint8_t> lens(316ull * nb);
-    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), nb));
-    auto work = [&](unsigned t) {
-      uint64_t fl[286], fd[30];
-      for (uint32_t b = t; b < nb; b += nt) {
-        for (int i = 0; i < 286; ++i) fl[i] = freq[316ull * b + i];
-        for (int i = 0; i < 30; ++i) fd[i] = freq[316ull * b + 286 + i];
-        uint8_t* l = lens.data() + 316ull * b;
-        host_package_merge(fl, 286, int(p->cwl), l);
-        host_package_merge(fd, 30, int(p->cwl), l + 286);
-        bool any = false;
-        for (int i = 0; i < 30; ++i) any |= l[286 + i] != 0;
-        if (!any) l[286] = 1;   // R14: one dummy distance code
-      }
-    };
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
-    work(0);
-    for (auto& t : th) t.join();
-    for (uint32_t b = 0; b < nb; ++b) {
-      const uint32_t ns = meta[4 * b];
-      S[b] = p->sub_block_seqs ? p->sub_block_seqs : (ns + p->sub_blocks_per_block - 1) / p->sub_blocks_per_block;
-      if (S[b] == 0) S[b] = 1;
-      nsub[b] = (ns + S[b] - 1) / S[b];
-      if (2ull * nsub[b] > Lw.sub_stride) return GOMP_ERR_INVALID_ARG;
-    }
+    // package-merge code lengths and the sub-block size S per block on the device (R14, R12)
+    pm_kernel<<<nb, 96, 0, st>>>(a, d_freq, ws + Lw.lens_off, reinterpret_cast<uint32_t*>(ws + Lw.sb_off), p->cwl,
+                                 p->sub_block_seqs, p->sub_blocks_per_block);
+    if (cudaGetLastError() != cudaSuccess) return GOMP_ERR_CUDA;
     uint8_t* d_lens = ws + Lw.lens_off;
     uint32_t* d_S = reinterpret_cast<uint32_t*>(ws + Lw.sb_off);
     uint32_t* d_sub = reinterpret_cast<uint32_t*>(ws + Lw.sub_off);
     uint8_t* d_pay = ws + Lw.pay_off;
-    if (cudaMemcpyAsync(d_lens, lens.data(), lens.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(d_S, S.data(), 4ull * nb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(d_sub, 0, 4 * Lw.sub_stride * nb, st) != cudaSuccess ||
+    if (cudaMemsetAsync(d_sub, 0, 4 * Lw.sub_stride * nb, st) != cudaSuccess ||
         cudaMemsetAsync(d_pay, 0, Lw.pay_stride * nb, st) != cudaSuccess)
       return GOMP_ERR_CUDA;
     huff_encode_kernel<<<nb, kCompThreads, 0, st>>>(a, d_lens, d_pay, Lw.pay_stride, d_sub, uint32_t(Lw.sub_stride), d_S);
     sub.resize(Lw.sub_stride * nb);
     if (cudaMemcpyAsync(sub.data(), d_sub, 4 * sub.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaMemcpyAsync(meta.data(), a.meta, 16ull * nb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(S.data(), d_S, 4ull * nb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
       return GOMP_ERR_CUDA;
+    for (uint32_t b = 0; b < nb; ++b) {
+      nsub[b] = (meta[4 * b] + S[b] - 1) / S[b];
+      if (2ull * nsub[b] > Lw.sub_stride) return GOMP_ERR_INVALID_ARG;   // cannot happen: sub_stride bounds it
+    }
   } else if (nb) {
     if (cudaMemcpyAsync(meta.data(), a.meta, 16ull * nb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
