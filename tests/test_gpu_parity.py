@@ -550,3 +550,32 @@ def test_or_copy_overread_bytes_discarded(nblocks, bs):
         for _ in range(5):
             y = _gpu(f, s).cpu().numpy()
             assert y.tobytes() == want, s
+
+
+@pytest.mark.parametrize("world,tiles", [(8, 8), (3, 4)])
+def test_bench_tiled_shards_full_size(world, tiles):
+    """bench.py's multi-GPU data at full C2 size (one GPU here: the ranks' shards decoded one after another on
+    cuda:0): the C2 file's blocks tiled `tiles` times, split by gomp_plan_shards, each rank's shard file
+    (bench.tiled_shard) decoded by the CUDA path; every byte equals the tiled input and sampled blocks the
+    oracle's decode of the shard."""
+    import bench
+    x = datagen.wiki(256 << 20, seed=2)
+    c = gomp.compress(x, mode="bit", de=True, block_size=262144, sub_blocks_per_block=16).numpy()
+    nb = gomp.get_info(c).n_blocks
+    first = gomp.plan_shards(bench.tiled_tables(c, tiles), world)
+    assert first[0] == 0 and first[-1] == nb * tiles
+    xd = torch.from_numpy(x).to(DEV)
+    bs = 262144
+    rng = np.random.default_rng(world)
+    for r in range(world):
+        b0, b1 = first[r], first[r + 1]
+        s = bench.tiled_shard(c, b0, b1)
+        y = _gpu(s)
+        assert y.numel() == (b1 - b0) * bs
+        for t in range(b0 // nb, (b1 - 1) // nb + 1):                   # every byte: pieces of the tiled input
+            j0, j1 = max(b0 - t * nb, 0), min(b1 - t * nb, nb)
+            o = (t * nb + j0 - b0) * bs
+            assert torch.equal(y[o:o + (j1 - j0) * bs], xd[j0 * bs:j1 * bs])
+        for b in rng.integers(b0, b1, 2):
+            ref = oracle.decompress_blocks(s, int(b) - b0, int(b) - b0 + 1, bs)
+            assert np.array_equal(y[(int(b) - b0) * bs:(int(b) - b0 + 1) * bs].cpu().numpy(), ref)
