@@ -533,8 +533,19 @@ __device__ __forceinline__ bool stage_bits(uint32_t stage_s, uint32_t cap, const
 // One CTA per data block; in round r thread t decodes sub-block r*T + t (used when sub-blocks are small, e.g.
 // the paper's 16-sequence sub-blocks, where there are thousands per block). The T sub-blocks of a
 // round are contiguous in the bitstream, so the round stages their bits in shared memory first.
+// A sub-block far longer than the round's mean (a DE file's first group of a block is nearly all literals:
+// C3 D=1 sub-blocks 0 and 1 carry ~26 kbit against a median of ~420) would hold its whole round on one lane;
+// it is deferred to the end of the round and decoded by a whole warp with the speculative decoder (K1b, G = 1).
+constexpr uint32_t kMaxHeavy = 16;          // deferred sub-blocks per round (more: decoded by their thread)
+constexpr uint32_t kHeavyMeanX = 8;         // deferred when bits >= this x the round's mean (and >= kSpecMinBits)
+constexpr uint32_t kRec = 64;
+constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below G*this use one lane (serial)
+template <bool LONG, uint32_t G, class RD>
+__device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Args& a, uint32_t vl, uint32_t bar, uint32_t recs_s,
+                          uint32_t xs_s, uint32_t b, uint32_t k, uint32_t S0, uint32_t bsz, uint32_t* rec,
+                          uint8_t* lit, uint32_t nseq, uint32_t nl, bool last);
 template <bool LONG>
-__global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t stage_cap) {
+__global__ void __launch_bounds__(256, 4) huff_thread_kernel(const Args a, uint32_t stage_cap) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
   uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
@@ -562,6 +573,12 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
   uint8_t* lit_base = tok + 4ull * e.n_seq;
   const uint8_t* gbits = pl + kTreeBytes;
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
+  // deferred (heavy) sub-blocks of the current round: {k, start bit, literal start, bits}; decoded by warps after
+  // the round with their recorded-iteration areas in the stage (free then), so only if the stage holds one
+  __shared__ uint4 heavy[kMaxHeavy];
+  __shared__ uint32_t n_heavy;
+  const uint32_t heavy_warps = min(nwarps, stage_cap / (32 * kRec));
+  if (tid == 0) n_heavy = 0;
   // a2: CTA-wide exclusive scans of the sub-block bit sizes and literal counts, round by round
   for (uint32_t c0 = 0; c0 < e.n_sub; c0 += blockDim.x) {
     const uint32_t k = c0 + tid;
@@ -588,12 +605,20 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
     if (tid == 0) { sm.carry_bits = tot_b; sm.carry_lits = tot_l; }
     const uint64_t start = pre_b + ib - bsz;
     const uint32_t lstart = pre_l + il - nl;
+    // heavy: at least kHeavyMeanX x the round's mean sub-block and long enough for the speculative decoder
+    const uint32_t in_round = min(blockDim.x, e.n_sub - c0);
+    const bool heavy_ok = heavy_warps != 0 && bsz >= kSpecMinBits && uint64_t(bsz) * in_round >= kHeavyMeanX * (tot_b - gs);
     if (k < e.n_sub) {
       uint32_t err = 0;
       if (start + bsz > bit_limit || uint64_t(lstart) + nl > e.n_lit) err = 1;
       const uint32_t seq0 = k * e.S;
       const uint32_t nseq = (k + 1 == e.n_sub) ? e.n_seq - seq0 : e.S;
-      if (!err) {
+      uint32_t hslot = kMaxHeavy;
+      if (!err && heavy_ok) {
+        hslot = atomicAdd(&n_heavy, 1u);
+        if (hslot < kMaxHeavy) heavy[hslot] = make_uint4(k, uint32_t(start), lstart, bsz);
+      }
+      if (!err && hslot >= kMaxHeavy) {
         err = staged ? decode_sub_serial<LONG>(srd, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq,
                                                nl, k + 1 == e.n_sub, bsz)
                      : decode_sub_serial<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a,
@@ -603,6 +628,24 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
     __syncthreads();
+    const uint32_t nh = min(n_heavy, kMaxHeavy);
+    if (nh) {
+      // the deferred sub-blocks, one warp each (bits from global memory: the stage now holds recorded iterations)
+      if (warp < heavy_warps) {
+        for (uint32_t h = warp; h < nh; h += heavy_warps) {
+          const uint4 q = heavy[h];
+          const uint32_t seq0 = q.x * e.S;
+          const bool last = q.x + 1 == e.n_sub;
+          const uint32_t nseq = last ? e.n_seq - seq0 : e.S;
+          const uint32_t* se = reinterpret_cast<const uint32_t*>(subt + uint64_t(kSubEntryBytes) * (e.sub_first + q.x));
+          group_sub<LONG, 1>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a, lane, 0u,
+                             stage_s + warp * (32 * kRec), 0u, b, q.x, q.y, q.w, rec_base + seq0, lit_base + q.z,
+                             nseq, __ldg(se + 1), last);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) n_heavy = 0;
+    }
   }
   if (tid == 0 && sm.carry_lits != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
 }
@@ -622,8 +665,6 @@ __global__ void __launch_bounds__(256) huff_thread_kernel(const Args a, uint32_t
 // Recorded iterations per lane (self-sync window): on text a lane started at a random bit needs p50 5, p99 ~37
 // symbols to join the true path; a lane that has not joined within its window costs its left neighbour a whole
 // extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
-constexpr uint32_t kRec = 64;
-constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below G*this use one lane (serial)
 constexpr uint32_t kWarpMinAvgBits = 8192;  // launcher: mean sub-block bits from which K1b is used
 constexpr uint32_t kHuffWarps = 16;         // warps per CTA (one data block; its groups share its sub-blocks)
 constexpr uint32_t kHuffG = 2;              // warps per sub-block group

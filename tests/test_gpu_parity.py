@@ -471,6 +471,72 @@ def test_forced_decoder_variant(kind, sub, huff):
     _check(c, x, ["auto"], huff=huff)
 
 
+def _heavy_data(n_units=54, seed=5, n_light=12):
+    """Units of one 16-sequence stretch of ~100 random literals per sequence (a ~13 kbit sub-block) followed by
+    n_light x 16 sequences of 64-byte matches of a periodic pattern (~150 bits each): a few sub-blocks per round
+    far longer than the mean, as a DE file's first group of every block (C3), here 19 of 256 in one round."""
+    rng = np.random.default_rng(seed)
+    period = rng.integers(0, 256, 61, dtype=np.uint8)
+    light = np.tile(period, n_light * 16 * 64 // 61 + 1)[:n_light * 16 * 64]
+    parts = []
+    for _ in range(n_units):
+        first = None
+        for _ in range(16):
+            r = rng.integers(0, 256, 100, dtype=np.uint8)
+            first = r if first is None else first
+            parts += [r, first[:8]]
+        parts.append(light)
+    return np.concatenate(parts)
+
+
+def _heavy_per_round(c):
+    """Deferred sub-blocks per thread-decoder round, by the kernel's rule (bits >= kSpecMinBits = 3072 and >= 8 x
+    the round's mean), with the launcher's round size for a grid of few blocks."""
+    a = np.asarray(c)
+    info = gomp.get_info(a)
+    t = a[64:64 + 32 * info.n_blocks].view(np.uint32).reshape(-1, 8)
+    sub = a[64 + 32 * info.n_blocks:64 + 32 * info.n_blocks + 8 * info.n_sub_total].view(np.uint32).reshape(-1, 2)
+    avg_sub = -(-info.n_sub_total // info.n_blocks)
+    nt = min(256, max(32, (avg_sub + 31) // 32 * 32))
+    res = []
+    for b in range(info.n_blocks):
+        bits = sub[t[b, 5]:t[b, 5] + t[b, 7], 0].astype(np.int64)
+        for r0 in range(0, len(bits), nt):
+            rb = bits[r0:r0 + nt]
+            res.append(int(((rb >= 3072) & (rb * len(rb) >= 8 * rb.sum())).sum()))
+    return res
+
+
+@pytest.mark.parametrize("de", [False, True])
+def test_thread_decoder_heavy_sub_blocks(de):
+    """Thread decoder rounds holding sub-blocks far longer than the mean: those are deferred and decoded by a whole
+    warp (speculative decoder, one warp); more than kMaxHeavy = 16 in one round (non-DE file: 19) leaves the rest
+    to their own thread. Same output as the oracle with either decoder; corrupted heavy sub-blocks are rejected
+    exactly when the oracle rejects them."""
+    x = _heavy_data()
+    c = gomp.compress(x, mode="bit", de=de, block_size=262144, sub_block_seqs=16)
+    per_round = _heavy_per_round(c)
+    assert max(per_round) > (16 if not de else 0), per_round
+    assert gomp.huff_variant(gomp.get_info(c)) == "thread"
+    _check(c, x, ["auto", "mrr"] if de else ["mrr"])
+    _check(c, x, ["auto"], huff="warp")
+    # 4 bit flips inside the first heavy sub-block of block 0, 16 times (the oracle rejects 8 / 5 of them)
+    import struct
+    a = np.asarray(c).copy()
+    info = gomp.get_info(a)
+    off = struct.unpack_from("<Q", a.tobytes(), 64)[0]
+    sub = a[64 + 32 * info.n_blocks:64 + 32 * info.n_blocks + 8 * info.n_sub_total].view(np.uint32).reshape(-1, 2)
+    k = int(np.flatnonzero(sub[:, 0] >= 3072)[0])
+    start = int(sub[:k, 0].astype(np.int64).sum())
+    lo = off + 160 + start // 8  # the 160-byte code-length header (kTreeBytes, FORMAT.md §3) precedes the bits
+    rng = np.random.default_rng(7)
+    seen = {}
+    for _ in range(16):
+        o_st, _ = _agree(_flip(a, rng, lo, lo + int(sub[k, 0]) // 8, 4), ("auto",))
+        seen[o_st] = seen.get(o_st, 0) + 1
+    assert sum(v for st, v in seen.items() if st != "ok") > 0, seen
+
+
 @pytest.mark.parametrize("mode", ["byte", "bit"])
 @pytest.mark.parametrize("n_dev", [1, 2, 3])
 def test_decompress_sharded(mode, n_dev):
