@@ -667,7 +667,9 @@ __global__ void __launch_bounds__(256, 4) huff_thread_kernel(const Args a, uint3
 // extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
 constexpr uint32_t kWarpMinAvgBits = 8192;  // launcher: mean sub-block bits from which K1b is used
 constexpr uint32_t kHuffWarps = 16;         // warps per CTA (one data block; its groups share its sub-blocks)
-constexpr uint32_t kHuffG = 2;              // warps per sub-block group
+constexpr uint32_t kHuffG = 2;              // warps per sub-block group for long sub-blocks (C2: ~48 kbit)
+constexpr uint32_t kHuffG2MinBits = 32768;  // launcher: mean sub-block bits from which groups of 2 warps are used
+                                            // (one warp per sub-block below: 8-32 kbit, measured on C5 shapes)
 constexpr uint32_t kXsBytes = 1024;         // per-group exchange area (shared memory)
 constexpr uint32_t kStageMax = 48 * 1024;   // largest per-group bit stage (bytes)
 constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per CTA
@@ -1736,26 +1738,30 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= kWarpMinAvgBits;
     const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
     if (use_warp) {
-      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of kHuffG warps per sub-block, speculative
-      // decode; per group a bit stage of 1.3x the mean sub-block (+ slack); up to kHuffWarps/kHuffG groups per
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of G warps per sub-block, speculative decode
+      // (G = 2 from ~32 kbit per sub-block; G = 1 below: C5 shapes, 256 MiB matrix, decode ms: 11 kbit 0.84-0.96
+      // vs 1.38-1.48, 22 kbit 0.74-0.79 vs 0.83-0.96, 44 kbit 1.00-1.11 vs 0.74-0.78, tools/crossover.py);
+      // per group a bit stage of 1.3x the mean sub-block (+ slack); up to kHuffWarps/G groups per
       // CTA, as many as the sub-blocks of a block and the shared memory allow
       // bit stage per group: 1.3x the mean sub-block (+ slack), but no more than lets two 16-warp CTAs share an SM
       // (a sub-block larger than the stage reads its bits from L1/L2 instead)
-      const uint64_t two_per_sm = ((kSmemPerSm / 2 - kSmemReservedPerCta - tabs) / (kHuffWarps / kHuffG) -
-                                   32 * kHuffG * kRec - kXsBytes) & ~uint64_t(15);
+      const uint32_t G = avg_bits >= kHuffG2MinBits ? kHuffG : 1u;
+      const uint64_t two_per_sm = ((kSmemPerSm / 2 - kSmemReservedPerCta - tabs) / (kHuffWarps / G) -
+                                   32 * G * kRec - kXsBytes) & ~uint64_t(15);
       const uint32_t cap = uint32_t(std::min<uint64_t>({kStageMax, align16(avg_bytes * 13 / 10 + 96),
                                                         std::max<uint64_t>(two_per_sm, align16(avg_bytes + 96))}));
-      const size_t slot = group_slot_bytes(kHuffG, cap);
+      const size_t slot = group_slot_bytes(G, cap);
       const uint64_t fit = (kSmemMax - tabs) / slot;
-      const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / kHuffG, fit, avg_sub})));
+      const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / G, fit, avg_sub})));
       const size_t smem = tabs + ngr * slot;
-      const auto kern = LONGc ? huff_warp_kernel<true, kHuffG> : huff_warp_kernel<false, kHuffG>;
+      const auto kern = G == 1 ? (LONGc ? huff_warp_kernel<true, 1> : huff_warp_kernel<false, 1>)
+                               : (LONGc ? huff_warp_kernel<true, kHuffG> : huff_warp_kernel<false, kHuffG>);
       ensure_smem(kern, smem);
       // split grid: blocks that fill at most half of the resident CTA slots are each decoded by two CTAs taking
       // half of its sub-blocks (the idle slots would otherwise wait out whole-block latencies; measured on the
       // first 74 blocks of C2: 0.095 vs 0.149 ms). Splitting only the last partial wave of a large grid was
       // measured as no gain (C2: 0.674 vs 0.675 ms).
-      const int occ = occupancy(kern, int(32 * kHuffG * ngr), smem);
+      const int occ = occupancy(kern, int(32 * G * ngr), smem);
       const uint32_t slots = uint32_t(std::max(occ, 0)) * sm_count();
       uint32_t grid = nblk;
       if (2 * uint64_t(nblk) <= slots && avg_sub >= 2 * uint64_t(ngr)) {
@@ -1763,7 +1769,7 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
         a.split_parts = 2;
         grid = 2 * nblk;
       }
-      kern<<<grid, 32 * kHuffG * ngr, smem, st>>>(a, cap);
+      kern<<<grid, 32 * G * ngr, smem, st>>>(a, cap);
     } else {
       // many short sub-blocks (e.g. the paper's 16 sequences per sub-block): one thread per sub-block, rounds
       // of nt sub-blocks staged together
