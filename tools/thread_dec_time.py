@@ -6,7 +6,9 @@ import torch, datagen, bench, paper_1606_00519_b200 as gomp
 files = {
     "C3-D1-bit": (datagen.nested(256 << 20, 1, seed=3), dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16)),
     "C3-D8-bit": (datagen.nested(256 << 20, 8, seed=3), dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16)),
+    "C3-D16-bit": (datagen.nested(256 << 20, 16, seed=3), dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16)),
     "C2-S16": (bench.gen("wiki", 256 << 20, 2), dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16)),
+    "C5-64k-S16": (datagen.matrix(256 << 20, seed=5), dict(mode="bit", de=True, block_size=65536, sub_block_seqs=16)),
 }
 comp = {k: (x, gomp.compress(x, **kw)) for k, (x, kw) in files.items()}
 for path in [gomp.LIB_PATH] + sorted(glob.glob("exp/*.so")):
