@@ -1,6 +1,7 @@
 """Dev helper: one decompression per kernel configuration, for compute-sanitizer (memcheck / racecheck /
 synccheck): Byte DE with the throughput and latency LZ77 copy variants, Bit with the speculative decoder
-(whole grid and split grid) and the thread decoder, MRR and SC on a non-DE file. Exits non-zero on a mismatch."""
+(whole grid and split grid, one- and two-warp groups) and the thread decoder (with long sub-blocks handed to
+one warp), MRR and SC on a non-DE file. Exits non-zero on a mismatch."""
 import sys
 sys.path.insert(0, '.')
 import numpy as np, torch, datagen, paper_1606_00519_b200 as gomp
@@ -10,6 +11,8 @@ cases = [
     ("bit warp 600 blocks", datagen.wiki(600 * 16384, seed=2), dict(mode="bit", de=True, block_size=16384, sub_blocks_per_block=2), "auto"),
     ("bit warp split", datagen.wiki(20 * 262144, seed=2), dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16), "auto"),
     ("bit thread S16", datagen.nested(2_000_000, 8, seed=3), dict(mode="bit", de=True, block_size=65536, sub_block_seqs=16), "auto"),
+    ("bit thread S16, long sub-blocks to one warp", datagen.nested(1_500_000, 1, seed=3), dict(mode="bit", de=True, block_size=262144, sub_block_seqs=16), "auto"),
+    ("bit warp G=1 (~12 kbit sub-blocks)", datagen.wiki(40 * 65536, seed=2), dict(mode="bit", de=True, block_size=65536, sub_blocks_per_block=16), "auto"),
     ("byte MRR", datagen.nested(1_000_000, 8, seed=3), dict(mode="byte", de=False, block_size=65536), "mrr"),
     ("byte SC", datagen.nested(500_000, 8, seed=3), dict(mode="byte", de=False, block_size=65536), "sc"),
 ]
