@@ -667,20 +667,26 @@ __global__ void __launch_bounds__(256, 4) huff_thread_kernel(const Args a, uint3
 // extra chunk, so the window is 64 (simulated warp pass-1 cost: 1.65x the mean chunk at 32, 1.31x at 64).
 constexpr uint32_t kWarpMinAvgBits = 8192;  // launcher: mean sub-block bits from which K1b is used
 constexpr uint32_t kHuffWarps = 16;         // warps per CTA (one data block; its groups share its sub-blocks)
-constexpr uint32_t kHuffG = 2;              // warps per sub-block group for long sub-blocks (C2: ~48 kbit)
-constexpr uint32_t kHuffG2MinBits = 32768;  // launcher: mean sub-block bits from which groups of 2 warps are used
-                                            // (one warp per sub-block below: 8-32 kbit, measured on C5 shapes)
-constexpr uint32_t kXsBytes = 1024;         // per-group exchange area (shared memory)
+constexpr uint32_t kHuffGMax = 8;           // warps per sub-block group: 1, 2, 4 or 8 (launcher)
+constexpr uint32_t kHuffG1Bits = 32768;     // launcher: G doubles every doubling of the mean sub-block from here
+                                            // (G = 1 below, 8 from 128 kbit; measured on C5 shapes)
 constexpr uint32_t kStageMax = 48 * 1024;   // largest per-group bit stage (bytes)
 constexpr size_t kSmemMax = 227 * 1024;     // opt-in dynamic shared memory per CTA
 constexpr size_t kSmemPerSm = 228 * 1024;   // shared memory per SM (B200)
 constexpr size_t kSmemReservedPerCta = 1024;
-// exchange area layout (bytes): [0, 8V) exit records; 768 sub-block index; 784.. per-warp aggregates
-constexpr uint32_t kXsK = 768, kXsAggA = 784, kXsAggB = 848, kXsAggC = 912, kXsNext = 960, kXsMbar = 1008;
-static_assert(8 * 32 * kHuffG <= kXsK && kHuffWarps % kHuffG == 0, "exchange area layout");
+// per-group exchange area (shared memory), bytes: [0, 8V) exit records (V = 32G lanes); the sub-block index;
+// per-warp aggregates A, B (8 bytes each), C and "next" flags (4 bytes each); the stage's mbarrier
+__host__ __device__ constexpr uint32_t xs_k(uint32_t G) { return 8 * 32 * G; }
+__host__ __device__ constexpr uint32_t xs_agga(uint32_t G) { return xs_k(G) + 16; }
+__host__ __device__ constexpr uint32_t xs_aggb(uint32_t G) { return xs_agga(G) + 8 * G; }
+__host__ __device__ constexpr uint32_t xs_aggc(uint32_t G) { return xs_aggb(G) + 8 * G; }
+__host__ __device__ constexpr uint32_t xs_next(uint32_t G) { return xs_aggc(G) + 4 * G; }
+__host__ __device__ constexpr uint32_t xs_mbar(uint32_t G) { return (xs_next(G) + 4 * G + 7) & ~7u; }
+__host__ __device__ constexpr uint32_t xs_bytes(uint32_t G) { return (xs_mbar(G) + 8 + 15) & ~15u; }
+static_assert(kHuffWarps % kHuffGMax == 0 && xs_bytes(kHuffGMax) <= 2304, "exchange area layout");
 
 __host__ __device__ constexpr uint32_t group_slot_bytes(uint32_t G, uint32_t stage_cap) {
-  return 32 * G * kRec + kXsBytes + stage_cap;
+  return 32 * G * kRec + xs_bytes(G) + stage_cap;
 }
 
 // group barrier (named barrier `bar`, 32G threads). __syncwarp first: the warp must arrive converged, or the
@@ -786,11 +792,11 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       sts64(xs_s + vl * 8, exit_vl | (exit_idx << 16), e_rel);
       // common case: every lane hands over to the next one (lane V-1 runs to the end), so every lane's true
       // segment starts at its predecessor's exit; otherwise follow the chain from lane 0, hop by hop
-      if (lane == 0) sts32(xs_s + kXsNext + wg * 4, __all_sync(FULL, exit_vl == vl + 1) ? 1u : 0u);
+      if (lane == 0) sts32(xs_s + xs_next(G) + wg * 4, __all_sync(FULL, exit_vl == vl + 1) ? 1u : 0u);
       else __all_sync(FULL, exit_vl == vl + 1);
       gsync<G>(bar);
       bool next_all = true;
-      for (uint32_t w = 0; w < G; ++w) next_all &= lds32(xs_s + kXsNext + w * 4) != 0;
+      for (uint32_t w = 0; w < G; ++w) next_all &= lds32(xs_s + xs_next(G) + w * 4) != 0;
       if (next_all) {
         if (vl == 0) {
           merged = 0;
@@ -843,10 +849,10 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       }
       uint32_t ph = 0, pv = 0;   // aggregate of the earlier warps of the group
       if (G > 1) {
-        if (lane == 31) sts64(xs_s + kXsAggA + wg * 8, hv, val);
+        if (lane == 31) sts64(xs_s + xs_agga(G) + wg * 8, hv, val);
         gsync<G>(bar);
         for (uint32_t w = 0; w < wg; ++w) {
-          const uint2 x = lds64(xs_s + kXsAggA + w * 8);
+          const uint2 x = lds64(xs_s + xs_agga(G) + w * 8);
           if (x.x) { ph = 1; pv = x.y; } else pv += x.y;
         }
         if (!hv) { hv = ph; val += pv; }
@@ -861,12 +867,12 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
     uint32_t seq_tot = __shfl_sync(FULL, seq_inc, 31), lit_tot = __shfl_sync(FULL, lit_inc, 31);
     bool tail_ok = __any_sync(FULL, is_tail && e_pos == bsz);
     if (G > 1) {
-      if (lane == 0) sts64(xs_s + kXsAggB + wg * 8, seq_tot | (tail_ok ? 0x80000000u : 0u), lit_tot);
+      if (lane == 0) sts64(xs_s + xs_aggb(G) + wg * 8, seq_tot | (tail_ok ? 0x80000000u : 0u), lit_tot);
       gsync<G>(bar);
       seq_tot = lit_tot = 0;
       tail_ok = false;
       for (uint32_t w = 0; w < G; ++w) {
-        const uint2 x = lds64(xs_s + kXsAggB + w * 8);
+        const uint2 x = lds64(xs_s + xs_aggb(G) + w * 8);
         if (w < wg) { seq_inc += x.x & 0x7fffffffu; lit_inc += x.y; }
         seq_tot += x.x & 0x7fffffffu;
         lit_tot += x.y;
@@ -914,9 +920,9 @@ __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Arg
       // R10: a literal run reaching 1023 closes a sequence, which the offsets above did not count
       serial = __any_sync(FULL, maxr >= kMaxLitRun);
       if (G > 1) {
-        if (lane == 0) sts32(xs_s + kXsAggC + wg * 4, serial ? 1u : 0u);
+        if (lane == 0) sts32(xs_s + xs_aggc(G) + wg * 4, serial ? 1u : 0u);
         gsync<G>(bar);
-        for (uint32_t w = 0; w < G; ++w) serial |= lds32(xs_s + kXsAggC + w * 4) != 0;
+        for (uint32_t w = 0; w < G; ++w) serial |= lds32(xs_s + xs_aggc(G) + w * 4) != 0;
       }
       if (!serial) {
         // the last lane of the last sub-block must end with EOB; EOB anywhere else is corrupt
@@ -951,7 +957,7 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t grp = warp / G, vl = tid % V, bar = 1 + grp;
   const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(lut_d + d_n)) + grp * group_slot_bytes(G, stage_cap);
-  const uint32_t recs_s = slot_s, xs_s = slot_s + V * kRec, stage_s = xs_s + kXsBytes;
+  const uint32_t recs_s = slot_s, xs_s = slot_s + V * kRec, stage_s = xs_s + xs_bytes(G);
   // in a split grid each CTA takes only a share of a block's sub-blocks (launcher)
   uint32_t bi = blockIdx.x, part = 0, parts = 1;
   if (bi >= a.split_first) {
@@ -975,7 +981,7 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
   const Luts t{lut_ll_s, lut_ll_s + ll_n * 4, ll_n - 1, d_n - 1, &sm};
   // the group's stage is filled by one TMA bulk copy per sub-block, completed on this mbarrier
-  const uint32_t mbar = xs_s + kXsMbar;
+  const uint32_t mbar = xs_s + xs_mbar(G);
   if (vl == 0) { mbar_init(mbar, 1); fence_mbar_init(); }
   __syncthreads();
   uint32_t phase = 0;
@@ -988,9 +994,9 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
   const uint64_t gmax = a.file_len - 16 - (e.payload_off + kTreeBytes);
   const uint8_t* gbits = pl + kTreeBytes;
   for (;;) {
-    if (vl == 0) sts32(xs_s + kXsK, k_lo + atomicAdd(&sm.next, 1u));
+    if (vl == 0) sts32(xs_s + xs_k(G), k_lo + atomicAdd(&sm.next, 1u));
     gsync<G>(bar);
-    const uint32_t k = lds32(xs_s + kXsK);
+    const uint32_t k = lds32(xs_s + xs_k(G));
     if (k >= k_hi) break;
     // a2: start bit and literal offset of sub-block k = sums over the entries before it (warp-parallel)
     uint64_t sb = 0;
@@ -1738,24 +1744,31 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= kWarpMinAvgBits;
     const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
     if (use_warp) {
-      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of G warps per sub-block, speculative decode
-      // (G = 2 from ~32 kbit per sub-block; G = 1 below: C5 shapes, 256 MiB matrix, decode ms: 11 kbit 0.84-0.96
-      // vs 1.38-1.48, 22 kbit 0.74-0.79 vs 0.83-0.96, 44 kbit 1.00-1.11 vs 0.74-0.78, tools/crossover.py);
+      // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of G warps per sub-block, speculative decode,
+      // G = 1 / 2 / 4 / 8 for mean sub-blocks below 32 / 64 / 128 kbit / above (C5 shapes, 256 MiB matrix,
+      // decode ms for G = 1, 2, 4, 8: 22 kbit 0.74-0.79, 0.83-0.96, -, -; 44 kbit 1.00-1.11, 0.75-0.78, 0.88-0.99,
+      // 1.66-1.95; 87 kbit -, 1.08-1.12, 0.77-0.82, 1.02-1.20; 174 kbit -, 1.43-1.64, 1.12-1.18, 0.81-0.90;
+      // 696 kbit -, 2.41, 1.97, 1.44; tools/crossover.py); C2's 48 kbit sub-blocks take G = 2;
       // per group a bit stage of 1.3x the mean sub-block (+ slack); up to kHuffWarps/G groups per
       // CTA, as many as the sub-blocks of a block and the shared memory allow
       // bit stage per group: 1.3x the mean sub-block (+ slack), but no more than lets two 16-warp CTAs share an SM
       // (a sub-block larger than the stage reads its bits from L1/L2 instead)
-      const uint32_t G = avg_bits >= kHuffG2MinBits ? kHuffG : 1u;
+      const uint32_t G = avg_bits < kHuffG1Bits ? 1u : avg_bits < 2 * kHuffG1Bits ? 2u : avg_bits < 4 * kHuffG1Bits ? 4u : 8u;
       const uint64_t two_per_sm = ((kSmemPerSm / 2 - kSmemReservedPerCta - tabs) / (kHuffWarps / G) -
-                                   32 * G * kRec - kXsBytes) & ~uint64_t(15);
+                                   32 * G * kRec - xs_bytes(G)) & ~uint64_t(15);
       const uint32_t cap = uint32_t(std::min<uint64_t>({kStageMax, align16(avg_bytes * 13 / 10 + 96),
                                                         std::max<uint64_t>(two_per_sm, align16(avg_bytes + 96))}));
       const size_t slot = group_slot_bytes(G, cap);
       const uint64_t fit = (kSmemMax - tabs) / slot;
       const uint32_t ngr = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>({kHuffWarps / G, fit, avg_sub})));
       const size_t smem = tabs + ngr * slot;
-      const auto kern = G == 1 ? (LONGc ? huff_warp_kernel<true, 1> : huff_warp_kernel<false, 1>)
-                               : (LONGc ? huff_warp_kernel<true, kHuffG> : huff_warp_kernel<false, kHuffG>);
+      void (*kern)(const Args, uint32_t) = nullptr;
+      switch (G) {
+        case 1: kern = LONGc ? huff_warp_kernel<true, 1> : huff_warp_kernel<false, 1>; break;
+        case 2: kern = LONGc ? huff_warp_kernel<true, 2> : huff_warp_kernel<false, 2>; break;
+        case 4: kern = LONGc ? huff_warp_kernel<true, 4> : huff_warp_kernel<false, 4>; break;
+        default: kern = LONGc ? huff_warp_kernel<true, 8> : huff_warp_kernel<false, 8>; break;
+      }
       ensure_smem(kern, smem);
       // split grid: blocks that fill at most half of the resident CTA slots are each decoded by two CTAs taking
       // half of its sub-blocks (the idle slots would otherwise wait out whole-block latencies; measured on the

@@ -441,10 +441,11 @@ def test_full_size_configs(cfg):
 
 
 @pytest.mark.parametrize("kind", ["wiki", "matrix", "nested2", "nested32", "random", "zeros", "text"])
-@pytest.mark.parametrize("k", [1, 4, 16, 40, 64])
+@pytest.mark.parametrize("k", [1, 4, 8, 16, 40, 64])
 def test_warp_speculative_decode(kind, k):
-    """Long sub-blocks (k per 256 KiB block) take the warp-per-sub-block speculative decoder; incompressible data
-    (1023-literal runs, R10) takes its serial fallback. Output must equal the oracle's bit for bit."""
+    """Long sub-blocks (k per 256 KiB block) take the speculative decoder with groups of 8, 4, 2 or 1 warps (by
+    the mean sub-block size: k = 1/4 -> 8, 8 -> 4, 16 -> 2, 40/64 -> 1 on text); incompressible data (1023-literal
+    runs, R10) takes its serial fallback. Output must equal the oracle's bit for bit."""
     x = _data(kind, 1_500_007, seed=13)
     c = gomp.compress(x, mode="bit", de=kind != "nested2", block_size=262144, sub_block_seqs=0, sub_blocks_per_block=k)
     _check(c, x, ["auto"])

@@ -5,6 +5,7 @@ import sys, statistics, glob
 sys.path.insert(0, '.')
 import torch, datagen, paper_1606_00519_b200 as gomp
 x = datagen.matrix(256 << 20, seed=5)
+xd = torch.from_numpy(x).cuda()
 cases = {}
 for bs in (65536, 262144, 1 << 20):
     for k in (4, 8, 16, 32, 64):
@@ -24,4 +25,6 @@ for path in [gomp.LIB_PATH] + sorted(glob.glob("exp/*.so")):
                 a.record(); gomp.decompress_into(info, d, out, ws, phase="decode", huff=huff); b.record(); torch.cuda.synchronize()
                 ts.append(a.elapsed_time(b))
             r[huff] = round(statistics.median(ts[2:]), 3)
-        print(path.split('/')[-1], key, "bits/sub", bits, "auto", gomp.huff_variant(info), r, flush=True)
+        gomp.decompress_into(info, d, out, ws, huff="warp")
+        ok = gomp.read_error(ws).status == 0 and torch.equal(out, xd)
+        print(path.split('/')[-1], key, "bits/sub", bits, "auto", gomp.huff_variant(info), r, "warp parity", ok, flush=True)
