@@ -619,6 +619,31 @@ def test_or_copy_overread_bytes_discarded(nblocks, bs):
             assert y.tobytes() == want, s
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("bs,sub", [(262144, "S16"), (1 << 20, 4), (65536, 16)])
+def test_c5_full_size(bs, sub):
+    """C5 at its BASELINE size as bench_configs.py measures it: a 256 MiB MatrixMarket-shaped file's blocks tiled
+    16x (4 GiB), one point per decoder (thread decoder with 16-sequence sub-blocks; speculative decoder with groups
+    of 8 warps for 1 MiB / 4 sub-blocks, of 1 warp for 64 KiB / 16): every byte vs the input, sampled blocks vs the
+    oracle."""
+    import bench
+    x = datagen.matrix(256 << 20, seed=5)
+    kw = dict(sub_block_seqs=16) if sub == "S16" else dict(sub_block_seqs=0, sub_blocks_per_block=sub)
+    c = gomp.compress(x, mode="bit", de=True, block_size=bs, **kw).numpy()
+    nb, tiles = gomp.get_info(c).n_blocks, 16
+    f = bench.tiled_shard(c, 0, nb * tiles)
+    y = _gpu(f)
+    xd = torch.from_numpy(x).to(DEV)
+    n = len(x)
+    assert y.numel() == n * tiles
+    for t in range(tiles):
+        assert torch.equal(y[t * n:(t + 1) * n], xd), t
+    rng = np.random.default_rng(bs)
+    for b in sorted(set([0, nb * tiles - 1] + [int(v) for v in rng.integers(0, nb * tiles, 4)])):
+        ref = oracle.decompress_blocks(f, b, b + 1, bs)
+        assert np.array_equal(y[b * bs:b * bs + len(ref)].cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("world,tiles", [(8, 8), (3, 4)])
 def test_bench_tiled_shards_full_size(world, tiles):
     """bench.py's multi-GPU data at full C2 size (one GPU here: the ranks' shards decoded one after another on
