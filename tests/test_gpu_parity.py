@@ -329,9 +329,10 @@ def test_blocks_range_and_shards():
 
 @pytest.mark.parametrize("mode", ["byte", "bit"])
 def test_lz77_copy_variants(mode):
-    """The DE LZ77 kernel has two copy variants chosen by grid size (grids of <= 3 CTAs per SM take
-    the latency variant): the same 600-block file decoded whole (throughput variant) and in 64-block ranges
-    (latency variant) must both equal the input and the oracle."""
+    """The DE LZ77 kernel has three variants chosen by grid size: 4-warp batches with the
+    instruction-lean copies (full grids), 4-warp batches with the load-first copies (<= 3 CTAs per SM) and 16-warp
+    batches (<= 1 CTA per SM). The same 600-block file decoded whole, in 300-block ranges and in 64-block ranges
+    must equal the input and the oracle."""
     x = datagen.wiki(600 * 65536 - 777, seed=12)
     c = gomp.compress(x, mode=mode, de=True, block_size=65536, sub_blocks_per_block=8)
     info = gomp.get_info(c)
@@ -340,12 +341,15 @@ def test_lz77_copy_variants(mode):
     d = c.to(DEV)
     out = torch.empty(info.uncompressed_len, dtype=torch.uint8, device=DEV)
     ws = torch.empty(gomp.workspace_size(info, 64), dtype=torch.uint8, device=DEV)
-    for b0 in range(0, 600, 64):
-        nb = min(64, 600 - b0)
-        gomp.decompress_into(info, d, out[b0 * 65536:], ws, first_block=b0, n_blocks=nb)
-        assert gomp.read_error(ws).status == 0
-    y = out.cpu().numpy()
-    assert np.array_equal(y, x)
+    ws = torch.empty(gomp.workspace_size(info, 300), dtype=torch.uint8, device=DEV)
+    for rng in (300, 64):
+        out.zero_()
+        for b0 in range(0, 600, rng):
+            nb = min(rng, 600 - b0)
+            gomp.decompress_into(info, d, out[b0 * 65536:], ws, first_block=b0, n_blocks=nb)
+            assert gomp.read_error(ws).status == 0
+        y = out.cpu().numpy()
+        assert np.array_equal(y, x), rng
     cn = c.numpy()
     for b in (0, 317, 599):
         ref = oracle.decompress_blocks(cn, b, b + 1, 65536)
@@ -597,14 +601,14 @@ def _edge_source_block(rng, block_size, window=8192):
     return seqs, bytes(lits)
 
 
-@pytest.mark.parametrize("nblocks,bs", [(3, 16384), (40, 4096), (2, 65536)])
+@pytest.mark.parametrize("nblocks,bs", [(3, 16384), (40, 4096), (2, 65536), (200, 4096), (600, 4096)])
 def test_or_copy_overread_bytes_discarded(nblocks, bs):
     """Directed test for the racecheck hazards of DESIGN.md §5: the OR-assembled word copies read up to 3 bytes on
     either side of a source range (the funnel-shift neighbours) and those bytes may be written concurrently by
     another lane or warp; they must never reach the output. Every source here ends 0-3 bytes before its group's
     start, so the over-read bytes are exactly the ones being written; run repeatedly, every strategy and copy
-    variant (40 blocks of 4 KiB: throughput copies; 2-3 blocks: the latency copies) must equal the sequential
-    expansion byte for byte."""
+    variant (600 blocks of 4 KiB: 4-warp batches, throughput copies; 200 blocks: 4-warp batches, load-first
+    copies; 2-40 blocks: 16-warp batches) must equal the sequential expansion byte for byte."""
     from fmt_util import expand
     rng = np.random.default_rng(bs + nblocks)
     blocks = [_edge_source_block(rng, bs) for _ in range(nblocks)]
