@@ -65,8 +65,6 @@ typedef enum {
  * one thread per sub-block (the paper's scheme); HUFF_WARP = one warp per sub-block, speculative. */
 #define GOMP_FLAG_HUFF_THREAD 0x800
 #define GOMP_FLAG_HUFF_WARP 0x1000
-/* HUFF_PAIR = two lanes per sub-block (one from its first bit, one from its middle), one decode pass */
-#define GOMP_FLAG_HUFF_PAIR 0x2000
 
 /* Compression parameters. Defaults (gomp_params_default) = the paper's setup. */
 typedef struct {
@@ -172,8 +170,7 @@ gomp_status gomp_get_info(const uint8_t* hdr, size_t hdr_len, gomp_info* out);
 gomp_status gomp_validate_tables(const uint8_t* file, size_t len, uint32_t* bad_block);
 
 /* Device workspace bytes needed to decompress n_blocks blocks of the file described by *info
- * (n_blocks = 0 means all). Bit files need, per block, a token buffer of max_block_tokens bytes and a decoder
- * scratch area of max_block_tokens + 24 KiB. */
+ * (n_blocks = 0 means all). Bit files need a token buffer of n_blocks * max_block_tokens bytes. */
 gomp_status gomp_decompress_workspace_size(const gomp_info* info, uint32_t n_blocks, size_t* bytes);
 
 /*

@@ -23,7 +23,6 @@ FLAG_DECODE_ONLY = 0x200
 FLAG_LZ77_ONLY = 0x400
 FLAG_HUFF_THREAD = 0x800
 FLAG_HUFF_WARP = 0x1000
-FLAG_HUFF_PAIR = 0x2000
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_MAGIC", -3: "UNSUPPORTED_VERSION", -4: "TRUNCATED",
           -5: "HEADER_INCONSISTENT", -6: "CORRUPT_STREAM", -7: "MALFORMED_BACKREF", -8: "NO_PROGRESS",
           -9: "DST_TOO_SMALL", -10: "WORKSPACE_TOO_SMALL", -11: "CUDA", -12: "OOM"}
@@ -212,7 +211,7 @@ def _stream_ptr(stream, device):
 def _strategy(strategy, stats, phase=None, huff=None):
     s = STRATEGIES[strategy] if isinstance(strategy, str) else int(strategy)
     s |= {None: 0, "decode": FLAG_DECODE_ONLY, "lz77": FLAG_LZ77_ONLY}[phase]
-    s |= {None: 0, "thread": FLAG_HUFF_THREAD, "warp": FLAG_HUFF_WARP, "pair": FLAG_HUFF_PAIR}[huff]
+    s |= {None: 0, "thread": FLAG_HUFF_THREAD, "warp": FLAG_HUFF_WARP}[huff]
     return s | (FLAG_STATS if stats else 0)
 
 
@@ -226,24 +225,19 @@ def token_bytes(c):
 
 
 def huff_variant(info):
-    """Which Bit decoder the launcher picks (mirrors decompress_range): "pair" when blocks hold at most 16
-    sub-blocks on average (kPairMaxSub) of 16 kbit to 1 Mbit (2 kPairMinBits, kPairMaxAvgBits), else "warp" when the
-    mean sub-block holds at least 8192 bits (kWarpMinAvgBits), else "thread"."""
+    """Which Bit decoder the launcher picks (mirrors decompress_range): "warp" when the mean sub-block holds at
+    least 8192 bits (kWarpMinAvgBits), else "thread"."""
     if not info.n_sub_total:
         return "thread"
-    avg_bits = (info.file_len - info.payload_base) * 8 // info.n_sub_total
-    avg_sub = -(-info.n_sub_total // max(info.n_blocks, 1))
-    if avg_sub <= 16 and 16384 <= avg_bits < (1 << 20):
-        return "pair"
-    return "warp" if avg_bits >= 8192 else "thread"
+    return "warp" if (info.file_len - info.payload_base) * 8 // info.n_sub_total >= 8192 else "thread"
 
 
 def decompress_into(info, src, dst, workspace, strategy="auto", stream=None, first_block=0, n_blocks=None,
                     stats=False, phase=None, huff=None):
     """Enqueue gomp_decompress(_blocks) on `stream` (no synchronisation). src/dst/workspace: CUDA uint8
     tensors; dst receives block first_block at dst[0]. phase="decode"/"lz77" runs one kernel of a Bit
-    decompression (profiling only, GOMP_FLAG_DECODE_ONLY / GOMP_FLAG_LZ77_ONLY); huff="thread"/"warp"/"pair"
-    forces the Bit decoder variant (testing, GOMP_FLAG_HUFF_THREAD / _WARP / _PAIR)."""
+    decompression (profiling only, GOMP_FLAG_DECODE_ONLY / GOMP_FLAG_LZ77_ONLY); huff="thread"/"warp"
+    forces the Bit decoder variant (testing, GOMP_FLAG_HUFF_THREAD / GOMP_FLAG_HUFF_WARP)."""
     for t in (src, dst, workspace):
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8 and t.is_contiguous()):
             raise ValueError("decompress_into needs contiguous CUDA uint8 tensors (no CPU fallback)")

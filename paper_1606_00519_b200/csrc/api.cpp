@@ -83,7 +83,7 @@ GOMP_EXPORT gomp_status gomp_decompress_workspace_size(const gomp_info* info, ui
   if (!info || !bytes) return GOMP_ERR_INVALID_ARG;
   const uint64_t nb = n_blocks ? n_blocks : info->n_blocks;
   uint64_t ws = kWsHeaderBytes;
-  if (info->mode == GOMP_MODE_BIT) ws += nb * bit_token_stride(info->max_block_tokens) + 64;
+  if (info->mode == GOMP_MODE_BIT) ws += nb * align16(info->max_block_tokens) + 64;
   *bytes = size_t(ws);
   return GOMP_OK;
 }

@@ -51,7 +51,7 @@ struct Args {
   uint8_t* dst;           // output of block first_block
   uint8_t* tokens;        // Bit: token buffer, block i of the range at tokens + i * tok_stride
   uint8_t* ws;            // workspace base (error word, stats)
-  uint64_t total, file_len, payload_base, tok_stride, scr_off;   // scr_off: K1c scratch within a block's stride
+  uint64_t total, file_len, payload_base, tok_stride;
   uint32_t first_block, n_blocks, block_size, window, min_match, max_match, cwl, ll_bits, d_bits, max_tok;
   uint32_t n_sub_total, nb_total, ring_bytes;
   // K1b split grid: CTAs from split_first on take 1/split_parts of a block's sub-blocks each
@@ -1041,353 +1041,6 @@ __global__ void __launch_bounds__(32 * kHuffWarps) huff_warp_kernel(const Args a
 }
 
 
-// ------------------------------------------------------------------ K1c: two lanes per sub-block, one pass (Bit)
-// For a few long sub-blocks per block (BASELINE C2: 16 x ~48 kbit per 256 KiB block). One warp per data block:
-// lane k (A) decodes sub-block k from its first bit, lane k+16 (B) from its middle bit, both in ONE pass that
-// writes tokens: A straight into the block's token buffer, B into a scratch area after it (its output offsets
-// depend on A's counts). B starts inside a codeword and decodes garbage until its path joins the true one
-// (canonical prefix codes self-synchronise, p99 ~37 symbols); it records the bit size and token counts of its
-// first kPairRec iterations. A stops at the first of B's recorded boundaries it lands on: from there both paths
-// are the same. B's tokens after that boundary are then copied behind A's (one record's literal run fixed), by
-// the whole warp. Each symbol is decoded once (plus A's short overrun) instead of twice (K1b's scan + writing
-// passes); 16 chains per block become 32 and the registers hold the bit window (no shared-memory stage).
-// Anything unusual after the join (a literal run near 1023 = R10, an invalid code, counts that do not add up,
-// no join within the window) is finished by the exact serial decoder from A's join point (or from the start),
-// which also reports corrupt streams: the same tokens as K1a/K1b, bit for bit.
-constexpr uint32_t kPairRec = 256;          // B's recorded iterations (join window)
-constexpr uint32_t kPairMinBits = 8192;     // shorter sub-blocks: lane A alone
-constexpr uint32_t kPairMaxSub = 16;        // sub-blocks per block handled as pairs (more: one lane each, serial)
-constexpr uint32_t kPairMaxAvgBits = 1u << 20;   // launcher: mean sub-block bits up to which K1c is chosen
-constexpr uint32_t kPairScrRec = kPairRec;  // scratch slack per sub-block: records, literals (garbage prefix)
-constexpr uint32_t kPairScrLit = 2 * kPairRec;
-// scratch bytes per block after its token buffer: B's records (4 B) and literals with the slack above
-static_assert(kPairScratchSlack == uint64_t(kPairMaxSub) * (4 * kPairScrRec + kPairScrLit), "format.hpp scratch");
-__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) { asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(uint16_t(v)) : "memory"); }
-__device__ __forceinline__ uint32_t lds16(uint32_t a) {
-  uint16_t v; asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory"); return v;
-}
-
-// symbol decode from a window (r0 = the next 32 stream bits, r1 = the 32 after them); as sym_decode
-template <bool LONG>
-__device__ __forceinline__ uint32_t sym_decode_w(uint32_t r0, uint32_t r1, const Luts& t, uint32_t& E, uint32_t& D,
-                                                 uint32_t& d32) {
-  E = ldsw(t.ll + ((r0 & t.mask_ll) << 2));
-  if (LONG && (E & 31u) == 0) {
-    const int sl = canon_slow(r0, t.sm->tab[0], t.sm->sorted_ll);
-    E = sl < 0 ? kBadLL : ll_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-  }
-  const uint32_t t1 = E & 31u;
-  d32 = __funnelshift_r(r0, r1, t1);
-  D = ldsw(t.d + ((d32 & t.mask_d) << 2));
-  const bool isl = ((E >> 9) & 3u) == K_LEN;
-  if (LONG && isl && (D & 31u) == 0) {
-    const int sl = canon_slow(d32, t.sm->tab[1], t.sm->sorted_d);
-    D = sl < 0 ? kBadD : d_entry(uint32_t(sl) & 0xffffu, uint32_t(sl) >> 16);
-  }
-  return t1 + (isl ? (D & 31u) : 0u);
-}
-
-template <bool LONG>
-__global__ void __launch_bounds__(32) huff_pair_kernel(const Args a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  HuffSmem& sm = *reinterpret_cast<HuffSmem*>(smem_raw);
-  uint32_t* lut_ll = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(HuffSmem) + 15) & ~size_t(15)));
-  const uint32_t ll_n = 1u << a.ll_bits, d_n = 1u << a.d_bits;
-  uint32_t* lut_d = lut_ll + ll_n;
-  const uint32_t recs_s = uint32_t(__cvta_generic_to_shared(lut_d + d_n));   // [kPairRec][16] u16 (B lanes)
-  const uint32_t lane = threadIdx.x, bi = blockIdx.x, b = a.first_block + bi;
-  const BlockEntry e = load_entry(a.src, b, lane);
-  if (!huff_block_ok(a, e, block_ulen(a, b))) {
-    if (lane == 0) report(a, GOMP_ERR_HEADER_INCONSISTENT, b, 0);
-    return;
-  }
-  const uint8_t* pl = a.src + e.payload_off;
-  if (!build_tables<LONG>(sm, lut_ll, lut_d, pl, a)) {
-    if (lane == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xffffffffull);
-    return;
-  }
-  const uint32_t lut_ll_s = uint32_t(__cvta_generic_to_shared(lut_ll));
-  const Luts t{lut_ll_s, lut_ll_s + ll_n * 4, ll_n - 1, d_n - 1, &sm};
-  const uint64_t bit_limit = uint64_t(e.payload_len - kTreeBytes) * 8;
-  const uint32_t* subt = reinterpret_cast<const uint32_t*>(a.src + kHeaderBytes + uint64_t(kBlockEntryBytes) * a.nb_total) +
-                         2ull * e.sub_first;
-  uint8_t* tok = a.tokens + uint64_t(bi) * a.tok_stride;
-  uint32_t* rec_base = reinterpret_cast<uint32_t*>(tok);
-  uint8_t* lit_base = tok + 4ull * e.n_seq;
-  const uint8_t* gbits = pl + kTreeBytes;
-  const uint32_t* g = reinterpret_cast<const uint32_t*>(gbits);
-  // last readable word and 16-byte chunk from g (16-aligned; the file continues >= 16 bytes past every payload)
-  const uint32_t gw_max = uint32_t((a.file_len - (e.payload_off + kTreeBytes)) / 4 - 1);
-  const uint32_t gc_max = (gw_max + 1) / 4 - 1;
-  const uint4* gc = reinterpret_cast<const uint4*>(gbits);
-  const uint32_t mm1 = a.min_match - 1, lrange = a.max_match - a.min_match, minm = a.min_match;
-
-  if (e.n_sub > kPairMaxSub) {
-    // more sub-blocks than pairs: one lane per sub-block, rounds of 32 (the paper's scheme, exact decoder)
-    uint64_t cb = 0;
-    uint32_t cl = 0;
-    for (uint32_t c0 = 0; c0 < e.n_sub; c0 += 32) {
-      const uint32_t k = c0 + lane;
-      const uint32_t bsz = k < e.n_sub ? __ldg(subt + 2 * k) : 0u, nl = k < e.n_sub ? __ldg(subt + 2 * k + 1) : 0u;
-      const uint64_t ib = warp_incl_scan_u64(bsz, lane);
-      const uint32_t il = warp_incl_scan_u32(nl, lane);
-      const uint64_t start = cb + ib - bsz;
-      const uint32_t lstart = cl + il - nl;
-      cb += __shfl_sync(FULL, ib, 31);
-      cl += __shfl_sync(FULL, il, 31);
-      if (k < e.n_sub) {
-        uint32_t err = 0;
-        if (start + bsz > bit_limit || uint64_t(lstart) + nl > e.n_lit) err = 1;
-        const uint32_t seq0 = k * e.S, last = k + 1 == e.n_sub;
-        const uint32_t nseq = last ? e.n_seq - seq0 : e.S;
-        if (!err)
-          err = decode_sub_serial<LONG>(GlobalBits{g}, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq,
-                                        nl, last, bsz);
-        if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
-      }
-    }
-    if (lane == 0 && cl != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
-    return;
-  }
-
-  // a2: start bit and literal offset of sub-block k = lane & 15 (both halves of the warp compute them)
-  const uint32_t k = lane & 15, half = lane >> 4;
-  const bool act = k < e.n_sub;
-  const uint32_t bsz = act ? __ldg(subt + 2 * k) : 0u, nl = act ? __ldg(subt + 2 * k + 1) : 0u;
-  uint64_t ib = bsz, il = nl;
-#pragma unroll
-  for (int d = 1; d < 16; d <<= 1) {
-    const uint64_t tb = __shfl_up_sync(FULL, ib, d, 16), tl = __shfl_up_sync(FULL, il, d, 16);
-    if (k >= uint32_t(d)) { ib += tb; il += tl; }
-  }
-  const uint64_t tot_l = __shfl_sync(FULL, il, 15, 16);
-  const uint64_t start64 = ib - bsz, lstart64 = il - nl;
-  const bool err = act && (start64 + bsz > bit_limit || lstart64 + nl > e.n_lit);
-  if (err && half == 0) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | 1u);
-  if (lane == 0 && tot_l != e.n_lit) report(a, GOMP_ERR_CORRUPT_STREAM, b, 0xfffffffeull);
-  const uint32_t S0 = uint32_t(start64), lstart = uint32_t(lstart64), endb = S0 + bsz;
-  const uint32_t seq0 = k * e.S;
-  const bool last = k + 1 == e.n_sub;
-  const uint32_t nseq = act ? (last ? e.n_seq - seq0 : e.S) : 0u;
-  const bool paired = act && !err && bsz >= kPairMinBits;
-  const uint32_t bstart = S0 + (bsz >> 1);
-  // outputs: A -> the token buffer, B -> scratch (sub-block k: records at k * (S + slack), literals after all
-  // records at lstart + k * slack)
-  uint8_t* scr = tok + a.scr_off;
-  uint32_t* recp;
-  uint8_t* litp;
-  uint32_t cap_r, cap_l;
-  if (half == 0) {
-    recp = rec_base + seq0;
-    litp = lit_base + lstart;
-    cap_r = nseq;
-    cap_l = nl;
-  } else {
-    recp = reinterpret_cast<uint32_t*>(scr) + uint64_t(k) * (e.S + kPairScrRec);
-    litp = scr + 4ull * (uint64_t(e.n_sub) * (e.S + kPairScrRec)) + lstart + uint64_t(k) * kPairScrLit;
-    cap_r = nseq + kPairScrRec;
-    cap_l = nl + kPairScrLit;
-  }
-  bool running = half == 0 ? (act && !err) : paired;
-  const bool pair_on = __shfl_sync(FULL, paired, k);   // A: is B decoding the second half
-  // bit window in registers: w0..w2 = stream words from base/32; the next words come from two 16-byte chunks
-  // loaded ahead (ca = the chunk holding the next word, at index j; cb = the one after it, in flight)
-  uint32_t at = half ? bstart : S0;
-  uint32_t base = at & ~31u;
-  const uint32_t wi = base >> 5;
-  uint32_t w0 = 0, w1 = 0, w2 = 0, j = (wi + 3) & 3u, cn = (wi + 3) >> 2;
-  uint4 ca = make_uint4(0u, 0u, 0u, 0u), cb = ca;
-  if (running) {
-    w0 = __ldg(g + min(wi, gw_max));
-    w1 = __ldg(g + min(wi + 1, gw_max));
-    w2 = __ldg(g + min(wi + 2, gw_max));
-    ca = __ldg(gc + min(cn, gc_max));
-    cb = __ldg(gc + min(cn + 1, gc_max));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(gc + min(cn + 8, gc_max)));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(gc + min(cn + 16, gc_max)));
-  }
-  uint32_t nrec = 0, nlit = 0, run = 0, iters = 0;
-  int spec_last = -1, spec_prev = -1;          // iterations of the two latest special symbols (bad code/EOB/range)
-  bool eob_last = false, overflow = false, synced = false;
-  uint32_t q = 0, bq = bstart, sync_j = 0;     // A: walk over B's recorded boundaries
-  const bool is_b = half != 0;
-  auto advance = [&]() {                       // at most twice (a symbol spans <= 48 bits)
-    while (at - base >= 32) {
-      w0 = w1;
-      w1 = w2;
-      w2 = j == 0 ? ca.x : j == 1 ? ca.y : j == 2 ? ca.z : ca.w;
-      base += 32;
-      if (++j == 4) {
-        j = 0;
-        ca = cb;
-        ++cn;
-        cb = __ldg(gc + min(cn + 1, gc_max));
-        // the line 2 lines ahead into L2 (the chunk loads then wait for L2, not for HBM)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(gc + min(cn + 17, gc_max)));
-      }
-    }
-  };
-  // one symbol, every rule (R10 pair split and close, EOB close, specials recorded, capped stores)
-  auto full_step = [&](bool record) {
-    const uint32_t rel = at - base;
-    const uint32_t r0 = __funnelshift_r(w0, w1, rel), r1 = __funnelshift_r(w1, w2, rel);
-    uint32_t E, D, d32;
-    uint32_t n = sym_decode_w<LONG>(r0, r1, t, E, D, d32);
-    const uint32_t kind = sym_kind(E);
-    const bool isl = kind == K_LEN, islit = kind == K_LIT;
-    uint32_t pair = islit ? sym_pair(E) : 0u;
-    const bool split = pair && run + 1 == kMaxLitRun;   // R10: the first literal closes the run, alone
-    if (split) { n = (E >> 5) & 15u; pair = 0; }
-    const uint32_t L = sym_len(E, r0);
-    const bool special = kind >= K_EOB || (isl && (((D >> 13) & 1u) || L - minm > lrange));
-    const uint32_t nli = islit ? 1u + pair : 0u;
-    if (islit && nlit < cap_l) litp[nlit] = uint8_t(E >> 16);
-    if (pair && nlit + 1 < cap_l) litp[nlit + 1] = uint8_t(E >> 24);
-    nlit += nli;
-    run += nli;
-    const bool r10 = islit && run == kMaxLitRun;
-    const bool close = isl || r10 || (kind == K_EOB && run != 0);
-    // B's records carry its running literal count (mod 1024) in the lit_len field; the copy turns it into runs
-    const uint32_t lfield = is_b ? (nlit & 1023u) : run;
-    if (close && nrec < cap_r) recp[nrec] = isl ? seq_record(lfield, L, sym_dist(D, d32), mm1) : lfield;
-    nrec += close ? 1u : 0u;
-    run = close ? 0u : run;
-    if (record) sts16(recs_s + (iters * 16 + k) * 2, n | (nli << 6) | (close ? 0x100u : 0u) | ((split || r10) ? 0x200u : 0u));
-    if (special) { spec_prev = spec_last; spec_last = int(iters); eob_last = kind == K_EOB; }
-    ++iters;
-    at += n;
-    advance();
-    overflow |= nrec > cap_r || nlit > cap_l;
-    return special;
-  };
-  // head: the first kPairRec symbols of every lane, B recording each (its garbage prefix tolerated)
-  for (uint32_t it = 0; it < kPairRec; ++it) {
-    if (!__any_sync(FULL, running)) break;
-    if (running) {
-      const bool sp = full_step(is_b);
-      if (at >= endb || overflow || (sp && !is_b)) running = false;
-    }
-  }
-  __syncwarp();                                // B's recorded window is visible to A from here on
-  // main: plain symbols only (lengths with valid ranges, literals away from R10, inside the caps); A up to B's
-  // start, B to the end; anything else leaves the loop to the per-lane tail below
-  {
-    const uint32_t lim = is_b ? endb : bstart;
-    while (running && at < lim && nrec < cap_r && nlit + 2 <= cap_l && run + 2 < kMaxLitRun) {
-      const uint32_t rel = at - base;
-      const uint32_t r0 = __funnelshift_r(w0, w1, rel), r1 = __funnelshift_r(w1, w2, rel);
-      const uint32_t E = ldsw(t.ll + ((r0 & t.mask_ll) << 2));
-      const uint32_t t1 = E & 31u, kind = sym_kind(E);
-      if (kind >= K_EOB || (LONG && t1 == 0)) break;
-      const uint32_t d32 = __funnelshift_r(r0, r1, t1);
-      const uint32_t D = ldsw(t.d + ((d32 & t.mask_d) << 2));
-      const bool isl = kind == K_LEN;
-      const uint32_t L = sym_len(E, r0);
-      if (isl && ((LONG && (D & 31u) == 0) || ((D >> 13) & 1u) || L - minm > lrange)) break;
-      const uint32_t pair = sym_pair(E);         // 0 for length entries
-      stg8_if(litp + nlit, E >> 16, !isl);
-      stg8_if(litp + nlit + 1, E >> 24, pair != 0);
-      const uint32_t lfield = is_b ? ((nlit + (isl ? 0u : 1u + pair)) & 1023u) : run;
-      stg32_if(recp + nrec, seq_record(lfield, L, sym_dist(D, d32), mm1), isl);
-      const uint32_t nli = isl ? 0u : 1u + pair;
-      nlit += nli;
-      run = isl ? 0u : run + nli;
-      nrec += isl ? 1u : 0u;
-      ++iters;
-      at += t1 + (isl ? (D & 31u) : 0u);
-      advance();
-    }
-  }
-  // tail: A walks B's recorded boundaries from B's start on and stops at the first it lands on (the join); B
-  // finishes its half; both with every rule
-  if (running && !is_b) {
-    for (;;) {
-      if (pair_on && at >= bstart && q < kPairRec) {
-        while (q < kPairRec && bq < at) { bq += lds16(recs_s + (q * 16 + k) * 2) & 63u; ++q; }
-        if (bq == at) { synced = true; sync_j = q; break; }
-      }
-      if (at >= endb || overflow) break;
-      if (full_step(false)) break;              // invalid code or EOB: the checks below decide
-    }
-  } else if (running) {
-    while (at < endb && !overflow) full_step(false);
-  }
-  running = false;
-  __syncwarp();
-  // ---------------- join: A's state to B (lane k -> k + 16)
-  const uint32_t a_sync = __shfl_sync(FULL, synced ? 1u : 0u, k), a_j = __shfl_sync(FULL, sync_j, k);
-  const uint32_t a_nrec = __shfl_sync(FULL, nrec, k), a_nlit = __shfl_sync(FULL, nlit, k);
-  const uint32_t a_run = __shfl_sync(FULL, run, k), a_at = __shfl_sync(FULL, at, k);
-  // B validates its segment [boundary a_j, end): counts before it and the literals up to its first record
-  bool b_ok = false;
-  uint32_t recs_j = 0, lits_j = 0;
-  if (half == 1 && paired && a_sync) {
-    bool ok = !overflow && at == endb;
-    for (uint32_t i = 0; i < a_j; ++i) {
-      const uint32_t f = lds16(recs_s + (i * 16 + k) * 2);
-      lits_j += (f >> 6) & 3u;
-      recs_j += (f >> 8) & 1u;
-    }
-    // literals from the join to B's first record there; no R10 event of B's (garbage-relative) run before it
-    uint32_t between = 0, r = a_j;
-    const uint32_t rlim = min(iters, kPairRec);
-    for (; r < rlim; ++r) {
-      const uint32_t f = lds16(recs_s + (r * 16 + k) * 2);
-      if (f & 0x200u) { ok = false; break; }
-      if (f & 0x100u) break;
-      between += (f >> 6) & 3u;
-    }
-    ok = ok && r < rlim && a_run + between < kMaxLitRun;
-    // specials after the join: only the block's closing EOB, as the very last symbol of the last sub-block
-    const bool fin = last && eob_last && spec_last == int(iters) - 1;
-    ok = ok && (fin ? spec_prev < int(a_j) : spec_last < int(a_j)) && (!last || fin);
-    ok = ok && a_nrec + (nrec - recs_j) == nseq && a_nlit + (nlit - lits_j) == nl;
-    b_ok = ok;
-  }
-  // A's own result when B did not take over: A ran to the end of the sub-block
-  bool a_done = false;
-  if (half == 0 && act && !err && !synced) {
-    const bool fin = last && eob_last && spec_last == int(iters) - 1;
-    a_done = !overflow && at == endb && (fin ? spec_prev < 0 : spec_last < 0) && (!last || fin) && nrec == nseq &&
-             nlit == nl;
-  }
-  const bool bok_k = __shfl_sync(FULL, b_ok, k + 16);
-  // ---------------- copy B's tokens after the join behind A's (whole warp, sub-block by sub-block)
-  uint32_t cm = __ballot_sync(FULL, b_ok) >> 16;
-  while (cm) {
-    const uint32_t s = __ffs(cm) - 1;
-    cm &= cm - 1;
-    const uint32_t src_lane = s + 16;
-    const uint32_t r_j = __shfl_sync(FULL, recs_j, src_lane), r_n = __shfl_sync(FULL, nrec, src_lane);
-    const uint32_t l_j = __shfl_sync(FULL, lits_j, src_lane), l_n = __shfl_sync(FULL, nlit, src_lane);
-    const uint32_t ar = __shfl_sync(FULL, a_nrec, src_lane), al = __shfl_sync(FULL, a_nlit, src_lane);
-    const uint32_t arun = __shfl_sync(FULL, a_run, src_lane);
-    const uint32_t ls = __shfl_sync(FULL, lstart, src_lane);
-    const uint32_t sq = s * e.S;
-    const uint32_t* srec = reinterpret_cast<const uint32_t*>(scr) + uint64_t(s) * (e.S + kPairScrRec);
-    const uint8_t* slit = scr + 4ull * (uint64_t(e.n_sub) * (e.S + kPairScrRec)) + ls + uint64_t(s) * kPairScrLit;
-    uint32_t* drec = rec_base + sq + ar;
-    uint8_t* dlit = lit_base + ls + al;
-    for (uint32_t i = r_j + lane; i < r_n; i += 32) {
-      const uint32_t v = srec[i];
-      const uint32_t prev = i == r_j ? (l_j - arun) : srec[i - 1];
-      drec[i - r_j] = (v & ~1023u) | ((v - prev) & 1023u);
-    }
-    for (uint32_t i = l_j + lane; i < l_n; i += 32) dlit[i - l_j] = slit[i];
-  }
-  // ---------------- anything else: the exact decoder, from A's join point (B's half) or from the start
-  if (half == 0 && act && !err && !a_done && !(synced && bok_k)) {
-    uint32_t e2;
-    if (synced)
-      e2 = decode_sub_exact<LONG>(GlobalBits{g}, t, a, a_at, S0, rec_base + seq0, lit_base + lstart, nseq, nl, last,
-                                  bsz, a_nrec, a_nlit, a_run, 0u);
-    else
-      e2 = decode_sub_exact<LONG>(GlobalBits{g}, t, a, S0, S0, rec_base + seq0, lit_base + lstart, nseq, nl, last, bsz,
-                                  0u, 0u, 0u, 0u);
-    if (e2) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | e2);
-  }
-}
-
 // ------------------------------------------------------------------ K2: warp-per-block LZ77 (+ Byte fusion)
 //
 // Output goes through a per-warp shared-memory ring holding the last RING bytes of the block (RING >= window
@@ -2072,7 +1725,7 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   const bool stats = (strategy & GOMP_FLAG_STATS) != 0;
   const bool decode_only = (strategy & GOMP_FLAG_DECODE_ONLY) != 0, lz77_only = (strategy & GOMP_FLAG_LZ77_ONLY) != 0;
   if (strategy & ~(GOMP_STRAT_MASK | GOMP_FLAG_STATS | GOMP_FLAG_DECODE_ONLY | GOMP_FLAG_LZ77_ONLY |
-                   GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP | GOMP_FLAG_HUFF_PAIR)) return GOMP_ERR_INVALID_ARG;
+                   GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP)) return GOMP_ERR_INVALID_ARG;
   if (decode_only && lz77_only) return GOMP_ERR_INVALID_ARG;
   if (s == GOMP_STRAT_AUTO) s = info->de ? GOMP_STRAT_DE : GOMP_STRAT_MRR;
   if (s != GOMP_STRAT_DE && s != GOMP_STRAT_MRR && s != GOMP_STRAT_SC) return GOMP_ERR_INVALID_ARG;
@@ -2092,12 +1745,11 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
   a.src = d_src;
   a.dst = d_dst;
   a.ws = static_cast<uint8_t*>(d_ws);
-  a.tokens = a.ws + kWsHeaderBytes + uint64_t(tok_block0) * bit_token_stride(info->max_block_tokens);
+  a.tokens = a.ws + kWsHeaderBytes + uint64_t(tok_block0) * align16(info->max_block_tokens);
   a.total = info->uncompressed_len;
   a.file_len = info->file_len;
   a.payload_base = info->payload_base;
-  a.tok_stride = bit_token_stride(info->max_block_tokens);
-  a.scr_off = align16(info->max_block_tokens);
+  a.tok_stride = align16(info->max_block_tokens);
   a.first_block = first;
   a.n_blocks = nblk;
   a.block_size = info->block_size;
@@ -2122,20 +1774,12 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
     const bool LONGc = info->cwl > kMaxLutBits;
     const size_t tabs = ((sizeof(HuffSmem) + 15) & ~size_t(15)) +
                         ((size_t(1) << a.ll_bits) + (size_t(1) << a.d_bits)) * sizeof(uint32_t);
-    const int force = strategy & (GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP | GOMP_FLAG_HUFF_PAIR);
+    const int force = strategy & (GOMP_FLAG_HUFF_THREAD | GOMP_FLAG_HUFF_WARP);
     // measured crossover (matrix data, 64 KiB-512 KiB blocks x 4-128 sub-blocks, profiles/r01_ncu_summary.md):
     // the speculative warp decoder wins from ~11 kbit sub-blocks up, the thread decoder below ~6 kbit
-    const bool use_pair = force ? force == GOMP_FLAG_HUFF_PAIR
-                                : avg_sub <= kPairMaxSub && avg_bits >= 2 * kPairMinBits && avg_bits < kPairMaxAvgBits;
     const bool use_warp = force ? force == GOMP_FLAG_HUFF_WARP : avg_bits >= kWarpMinAvgBits;
     const uint64_t avg_bytes = avg_bits / 8 + 1;   // mean sub-block payload bytes
-    if (use_pair) {
-      // few long sub-blocks (C2): one warp per block, two lanes per sub-block, one decode pass
-      const size_t smem = tabs + size_t(kPairRec) * 16 * 2;
-      const auto kern = LONGc ? huff_pair_kernel<true> : huff_pair_kernel<false>;
-      ensure_smem(kern, smem);
-      kern<<<nblk, 32, smem, st>>>(a);
-    } else if (use_warp) {
+    if (use_warp) {
       // few long sub-blocks (e.g. C2: 16 per 256 KiB block): a group of G warps per sub-block, speculative decode,
       // G = 1 / 2 / 4 / 8 for mean sub-blocks below 32 / 64 / 128 kbit / above (C5 shapes, 256 MiB matrix,
       // decode ms for G = 1, 2, 4, 8: 22 kbit 0.74-0.79, 0.83-0.96, -, -; 44 kbit 1.00-1.11, 0.75-0.78, 0.88-0.99,

@@ -18,11 +18,6 @@ constexpr uint32_t kMaxLitRun = 1023;  // reading R10
 constexpr size_t kWsHeaderBytes = 1024;  // workspace: error word + stats, then the token buffer
 
 inline uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
-// Bit files: per-block stride of the workspace token area = the block's token buffer + the K1c decoder's scratch
-// (the second lane of each sub-block pair writes there first; decode.cu, huff_pair_kernel): max_tok plus, per
-// sub-block (<= 16), 256 records and 512 literals of slack for its speculative prefix
-constexpr uint64_t kPairScratchSlack = 16 * (4 * 256 + 512);
-inline uint64_t bit_token_stride(uint64_t max_tok) { return align16(max_tok) + align16(max_tok + kPairScratchSlack); }
 inline uint32_t ld32(const uint8_t* p) { uint32_t v; std::memcpy(&v, p, 4); return v; }
 inline uint64_t ld64(const uint8_t* p) { uint64_t v; std::memcpy(&v, p, 8); return v; }
 inline void st32(uint8_t* p, uint32_t v) { std::memcpy(p, &v, 4); }
