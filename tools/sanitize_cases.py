@@ -1,5 +1,6 @@
 """Dev helper: one decompression per kernel configuration, for compute-sanitizer (memcheck / racecheck /
-synccheck): Byte DE with the throughput and latency LZ77 copy variants, Bit with the speculative decoder
+synccheck): Byte DE with the three LZ77 variants (4-warp batches with instruction-lean or load-first copies,
+16-warp batches), Bit with the speculative decoder
 (whole grid and split grid, one- and two-warp groups) and the thread decoder (with long sub-blocks handed to
 one warp), MRR and SC on a non-DE file. Exits non-zero on a mismatch."""
 import sys
@@ -7,7 +8,8 @@ sys.path.insert(0, '.')
 import numpy as np, torch, datagen, paper_1606_00519_b200 as gomp
 cases = [
     ("byte DE 537 blocks", datagen.wiki(2_200_000, seed=21), dict(mode="byte", de=True, block_size=4096), "auto"),
-    ("byte DE 19 blocks", datagen.wiki(300_000, seed=21), dict(mode="byte", de=True, block_size=16384), "auto"),
+    ("byte DE 19 blocks (16-warp batches)", datagen.wiki(300_000, seed=21), dict(mode="byte", de=True, block_size=16384), "auto"),
+    ("byte DE 300 blocks (load-first copies)", datagen.wiki(300 * 4096, seed=21), dict(mode="byte", de=True, block_size=4096), "auto"),
     ("bit warp 600 blocks", datagen.wiki(600 * 16384, seed=2), dict(mode="bit", de=True, block_size=16384, sub_blocks_per_block=2), "auto"),
     ("bit warp split", datagen.wiki(20 * 262144, seed=2), dict(mode="bit", de=True, block_size=262144, sub_blocks_per_block=16), "auto"),
     ("bit thread S16", datagen.nested(2_000_000, 8, seed=3), dict(mode="bit", de=True, block_size=65536, sub_block_seqs=16), "auto"),
