@@ -265,6 +265,31 @@ struct GlobalBits {
     r1 = __funnelshift_r(w1, w2, at);
   }
 };
+// GlobalBits with the window kept in registers while one thread reads forward (the thread decoder's unstaged
+// rounds): three stream words and the next one loaded ahead, so a symbol costs no load on its dependence chain
+// (one load per 32 bits consumed). Word indices are clamped to `last`, the stream's readable end.
+struct RegGlobalBits {
+  const uint32_t* g;
+  uint32_t last, wi, w0, w1, w2, nx;   // w0 = word wi
+  __device__ __forceinline__ RegGlobalBits(const uint32_t* gp, uint32_t last_word, uint32_t at) : g(gp), last(last_word) {
+    wi = at >> 5;
+    w0 = __ldg(g + min(wi, last));
+    w1 = __ldg(g + min(wi + 1, last));
+    w2 = __ldg(g + min(wi + 2, last));
+    nx = __ldg(g + min(wi + 3, last));
+  }
+  __device__ __forceinline__ void window(uint32_t at, uint32_t& r0, uint32_t& r1) {
+    while (wi < (at >> 5)) {         // 0, 1 or 2 steps (a symbol spans <= 48 bits); positions only grow
+      w0 = w1;
+      w1 = w2;
+      w2 = nx;
+      ++wi;
+      nx = __ldg(g + min(wi + 3, last));
+    }
+    r0 = __funnelshift_r(w0, w1, at);
+    r1 = __funnelshift_r(w1, w2, at);
+  }
+};
 
 struct Luts {
   uint32_t ll, d, mask_ll, mask_d;   // shared-window addresses of the two tables, index masks
@@ -275,7 +300,7 @@ struct Luts {
 // bits, and for a length code the distance entry D and its extra bits. Returns the bits it spans (>= 1; a
 // K_BAD entry spans 1 bit so that speculative lanes always progress). r0/d32 are kept for value extraction.
 template <bool LONG, class RD>
-__device__ __forceinline__ uint32_t sym_decode(const RD& rd, uint32_t at, const Luts& t, uint32_t& E, uint32_t& D,
+__device__ __forceinline__ uint32_t sym_decode(RD&& rd, uint32_t at, const Luts& t, uint32_t& E, uint32_t& D,
                                                uint32_t& r0, uint32_t& d32) {
   uint32_t r1;
   rd.window(at, r0, r1);
@@ -432,7 +457,7 @@ __device__ __forceinline__ void stg32_if(uint32_t* p, uint32_t v, bool c) {
 // Exact serial decode of a sub-block's remaining symbols from bit `at` (state si, lw, run, bad carried in):
 // records at rec[0..nseq), literals at lit[0..nl). Returns 0 or a CorruptStream detail code.
 template <bool LONG, class RD>
-__device__ uint32_t decode_sub_exact(const RD& rd, const Luts& t, const Args& a, uint32_t at, uint32_t b0, uint32_t* rec,
+__device__ uint32_t decode_sub_exact(RD&& rd, const Luts& t, const Args& a, uint32_t at, uint32_t b0, uint32_t* rec,
                                      uint8_t* lit, uint32_t nseq, uint32_t nl, bool last, uint32_t bsz, uint32_t si,
                                      uint32_t lw, uint32_t run, uint32_t bad) {
   const uint32_t mm1 = a.min_match - 1;
@@ -481,7 +506,7 @@ __device__ uint32_t decode_sub_exact(const RD& rd, const Luts& t, const Args& a,
 // literal count limits, a code longer than the table — and the exact loop above finishes from that symbol
 // boundary, so every check and every result is the exact loop's.
 template <bool LONG, class RD>
-__device__ uint32_t decode_sub_serial(const RD& rd, const Luts& t, const Args& a, uint32_t at, uint32_t* rec,
+__device__ uint32_t decode_sub_serial(RD&& rd, const Luts& t, const Args& a, uint32_t at, uint32_t* rec,
                                       uint8_t* lit, uint32_t nseq, uint32_t nl, bool last, uint32_t bsz) {
   const uint32_t mm1 = a.min_match - 1, lrange = a.max_match - a.min_match, b0 = at;
   uint32_t si = 0, lw = 0, run = 0, bad = 0;
@@ -543,6 +568,7 @@ __device__ __forceinline__ bool stage_bits(uint32_t stage_s, uint32_t cap, const
 constexpr uint32_t kMaxHeavy = 16;          // deferred sub-blocks per round (more: decoded by their thread)
 constexpr uint32_t kHeavyMeanX = 8;         // deferred when bits >= this x the round's mean (and >= kSpecMinBits)
 constexpr uint32_t kRec = 64;
+constexpr uint32_t kThreadNoStageThreads = 32;   // launcher: thread-decoder CTAs up to this size stage no bits
 constexpr uint32_t kSpecMinBits = 32 * 96;  // sub-blocks below G*this use one lane (serial)
 template <bool LONG, uint32_t G, class RD>
 __device__ __forceinline__ void group_sub(const RD& rd, const Luts& t, const Args& a, uint32_t vl, uint32_t bar, uint32_t recs_s,
@@ -623,11 +649,17 @@ __global__ void __launch_bounds__(256, 4) huff_thread_kernel(const Args a, uint3
         if (hslot < kMaxHeavy) heavy[hslot] = make_uint4(k, uint32_t(start), lstart, bsz);
       }
       if (!err && hslot >= kMaxHeavy) {
-        err = staged ? decode_sub_serial<LONG>(srd, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq,
-                                               nl, k + 1 == e.n_sub, bsz)
-                     : decode_sub_serial<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a,
-                                               uint32_t(start), rec_base + seq0, lit_base + lstart, nseq, nl,
-                                               k + 1 == e.n_sub, bsz);
+        if (staged) {
+          err = decode_sub_serial<LONG>(srd, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq, nl,
+                                        k + 1 == e.n_sub, bsz);
+        } else if (stage_cap) {   // a round larger than the stage: its bits straight from L1/L2
+          err = decode_sub_serial<LONG>(GlobalBits{reinterpret_cast<const uint32_t*>(gbits)}, t, a, uint32_t(start),
+                                        rec_base + seq0, lit_base + lstart, nseq, nl, k + 1 == e.n_sub, bsz);
+        } else {                  // no stage (one-warp CTAs, launcher): the window in registers
+          RegGlobalBits rg(reinterpret_cast<const uint32_t*>(gbits), uint32_t((gmax + 16) / 4 - 1), uint32_t(start));
+          err = decode_sub_serial<LONG>(rg, t, a, uint32_t(start), rec_base + seq0, lit_base + lstart, nseq, nl,
+                                        k + 1 == e.n_sub, bsz);
+        }
       }
       if (err) report(a, GOMP_ERR_CORRUPT_STREAM, b, (uint64_t(k) << 8) | err);
     }
@@ -1828,7 +1860,11 @@ gomp_status decompress_range(const gomp_info* info, uint32_t first, uint32_t nbl
       // 128 threads lose 21%)
       const uint32_t nt_max = nblk >= 6 * sm_count() ? 128u : 256u;
       const uint32_t nt = uint32_t(std::min<uint64_t>(nt_max, std::max<uint64_t>(32, (avg_sub + 31) / 32 * 32)));
-      const uint32_t cap = uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * nt * 3 / 2 + 512)));
+      // one-warp CTAs (<= 32 sub-blocks per block) stage nothing: their round's stage (the whole block's bits x 1.5)
+      // would hold an SM to 4-5 such CTAs; each thread keeps its window in registers and reads the bits through
+      // L1 instead (C5 64 KiB x 32 sub-blocks: decode 1.48 -> 1.18 ms per 256 MiB; 64 threads: 1.14 -> 1.16,
+      // so larger CTAs keep the stage)
+      const uint32_t cap = nt <= kThreadNoStageThreads ? 0u : uint32_t(std::min<uint64_t>(kStageMax, align16(avg_bytes * nt * 3 / 2 + 512)));
       const size_t smem = tabs + cap;
       if (LONGc) {
         ensure_smem(huff_thread_kernel<true>, smem);

@@ -189,7 +189,7 @@ def test_device_errors_byte():
 FORMAT_ERRORS = ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT")
 
 
-def _agree(f, strategies=("auto",)):
+def _agree(f, strategies=("auto",), huff=None):
     """Run f through the oracle and the GPU (each strategy); returns (oracle status or 'ok', gpu statuses)."""
     try:
         ref, o_st = oracle.decompress(f), "ok"
@@ -198,7 +198,7 @@ def _agree(f, strategies=("auto",)):
     g_sts = []
     for s in strategies:
         try:
-            y, g_st = _gpu(f, s).cpu().numpy(), "ok"
+            y, g_st = _gpu(f, s, huff=huff).cpu().numpy(), "ok"
         except gomp.GompError as e:
             y, g_st = None, e.name
         assert (o_st == "ok") == (g_st == "ok"), f"strategy {s}: oracle {o_st}, gpu {g_st}"
@@ -218,11 +218,12 @@ def _flip(c, rng, lo, hi, n):
     return bad
 
 
-@pytest.mark.parametrize("sub", [("k", 8), ("S", 16)])
-def test_device_errors_bit_fuzz(sub):
+@pytest.mark.parametrize("sub,huff", [(("k", 8), None), (("S", 16), None), (("k", 8), "thread")])
+def test_device_errors_bit_fuzz(sub, huff):
     """Bit flips in Bit payloads (trees, bitstreams), block-table and sub-table entries: GPU raises iff the
     oracle does, identical output otherwise. k=8 sub-blocks of ~3 kbit per block go through the speculative
-    warp decoder, S=16 through the thread decoder."""
+    warp decoder, S=16 through the thread decoder with staged rounds, k=8 forced onto the thread decoder through
+    its one-warp CTAs that stage nothing (register window)."""
     import struct
     x = datagen.wiki(200_000, seed=2)
     kw = dict(sub_block_seqs=0, sub_blocks_per_block=sub[1]) if sub[0] == "k" else dict(sub_block_seqs=sub[1])
@@ -234,7 +235,7 @@ def test_device_errors_bit_fuzz(sub):
     regions = [(off, off + 3000), (off, len(c) - 16), (64, 64 + 32 * info.n_blocks), (64 + 32 * info.n_blocks, off)]
     for i in range(80):
         lo, hi = regions[i % len(regions)]
-        o_st, g = _agree(_flip(c, rng, lo, hi, int(rng.integers(1, 3))), ("auto", "mrr"))
+        o_st, g = _agree(_flip(c, rng, lo, hi, int(rng.integers(1, 3))), ("auto", "mrr"), huff=huff)
         seen[o_st] = seen.get(o_st, 0) + 1
     assert seen.get("CORRUPT_STREAM", 0) > 0, seen
     bad = c.copy()
