@@ -6,8 +6,8 @@
 //       P:656-659; literal-pair entries); a4 sub-block decode, one table lookup per symbol, into Byte-format
 //       records and literals in the workspace token buffer: K1a one thread per sub-block (the
 //       paper's scheme), K1b 64 lanes per sub-block with self-synchronising speculative starts.
-//   lz77_batch_kernel (K2b)  the DE strategy: 4 warps per data block take 4 consecutive 32-sequence groups, one
-//       sequence per lane: a5 record + one packed warp exclusive scan giving both prefix sums
+//   lz77_batch_kernel (K2b)  the DE strategy: BW warps per data block (4; 16 for grids of at most one CTA per SM)
+//       take BW consecutive 32-sequence groups, one sequence per lane: a5 record + one packed warp exclusive scan giving both prefix sums
 //       (P:105-112); a6 literal copy; a7 back-references in one round (Dependency Elimination,
 //       P:295-329). For Gompresso/Byte the records come straight from the file (a8, single pass).
 //   lz77_kernel<STRAT> (K2)  one warp per data block: Multi-Round Resolution (Fig. alg:mrr,
@@ -31,15 +31,15 @@ namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t kPipeStreams = 4;     // compute streams of the pipelined host path
-constexpr uint32_t kPipeMaxChunks = 12;
+constexpr uint32_t kPipeMaxChunks = 12;  // chunks of the pipelined host path (sizes double: small first chunks)
 #ifndef GOMP_LOWLAT_CTAS_PER_SM
 #define GOMP_LOWLAT_CTAS_PER_SM 3
 #endif
 #ifndef GOMP_LAT_CTAS_PER_SM
 #define GOMP_LAT_CTAS_PER_SM 1
 #endif
-constexpr uint32_t kLatCtasPerSm = GOMP_LAT_CTAS_PER_SM;         // LZ77 grids up to this many CTAs per SM: 16-warp batches
-constexpr uint32_t kLowLatCtasPerSm = GOMP_LOWLAT_CTAS_PER_SM;   // LZ77 grids up to this many CTAs per SM use or_copy_ll  // chunks of the pipelined host path (sizes double: small first chunks)
+constexpr uint32_t kLatCtasPerSm = GOMP_LAT_CTAS_PER_SM;         // DE LZ77 grids up to this many CTAs per SM: 16-warp batches
+constexpr uint32_t kLowLatCtasPerSm = GOMP_LOWLAT_CTAS_PER_SM;   // ... up to this many: 4-warp batches, or_copy_ll copies
 constexpr int kLz77Warps = 2;        // warps (= data blocks) per CTA of the LZ77 kernel
 constexpr int kMaxLutBits = 11;      // LUT index width = min(cwl, 11); longer codes take the canonical path
 
