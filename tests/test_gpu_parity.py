@@ -625,12 +625,12 @@ def test_or_copy_overread_bytes_discarded(nblocks, bs):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("bs,sub", [(262144, "S16"), (1 << 20, 4), (65536, 16)])
+@pytest.mark.parametrize("bs,sub", [(262144, "S16"), (1 << 20, 4), (65536, 16), (65536, 32)])
 def test_c5_full_size(bs, sub):
     """C5 at its BASELINE size as bench_configs.py measures it: a 256 MiB MatrixMarket-shaped file's blocks tiled
     16x (4 GiB), one point per decoder (thread decoder with 16-sequence sub-blocks; speculative decoder with groups
-    of 8 warps for 1 MiB / 4 sub-blocks, of 1 warp for 64 KiB / 16): every byte vs the input, sampled blocks vs the
-    oracle."""
+    of 8 warps for 1 MiB / 4 sub-blocks, of 1 warp for 64 KiB / 16; the stage-less one-warp thread decoder for
+    64 KiB / 32): every byte vs the input, sampled blocks vs the oracle."""
     import bench
     x = datagen.matrix(256 << 20, seed=5)
     kw = dict(sub_block_seqs=16) if sub == "S16" else dict(sub_block_seqs=0, sub_blocks_per_block=sub)
