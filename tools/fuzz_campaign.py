@@ -6,7 +6,10 @@ table), decode the corrupted file with the oracle and on the GPU (launcher's cho
 strategy that applies), and require the GPU to fail iff the oracle fails, with identical output when both accept.
 Prints one JSON line of counts; exits non-zero on the first disagreement (after printing it).
 
-usage: python tools/fuzz_campaign.py [seconds] [seed]
+With --clean: no corruption, inputs up to 64 blocks of up to 1 MiB (full grids of every kernel variant), every
+output compared with the oracle's.
+
+usage: python tools/fuzz_campaign.py [seconds] [seed] [--clean]
 """
 import json
 import struct
@@ -22,8 +25,10 @@ import oracle
 import paper_1606_00519_b200 as gomp
 
 FORMAT_ERRORS = ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT")
-seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
-rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+clean = "--clean" in sys.argv
+argv = [v for v in sys.argv if v != "--clean"]
+seconds = float(argv[1]) if len(argv) > 1 else 300.0
+rng = np.random.default_rng(int(argv[2]) if len(argv) > 2 else 0)
 KINDS = ["wiki", "text", "matrix", "random", "zeros", "nested2", "nested8"]
 
 
@@ -49,8 +54,10 @@ while time.time() - t0 < seconds:
     kind = KINDS[int(rng.integers(len(KINDS)))]
     mode = "bit" if rng.random() < 0.6 else "byte"
     de = bool(rng.random() < 0.7) and kind != "nested2"
-    bs = int(rng.choice([4096, 16384, 65536, 262144]))
-    n = int(rng.integers(1, 8)) * bs - int(rng.integers(0, bs))
+    bs = int(rng.choice([4096, 16384, 65536, 262144] + ([1 << 20] if clean else [])))
+    n = int(rng.integers(1, 65 if clean else 8)) * bs - int(rng.integers(0, bs))
+    if clean:
+        n = min(n, 48 << 20)
     kw = dict(mode=mode, de=de, block_size=bs)
     if mode == "bit":
         if rng.random() < 0.5:
@@ -72,7 +79,7 @@ while time.time() - t0 < seconds:
     if hi <= lo:
         continue
     f = c.copy()
-    for _ in range(int(rng.integers(1, 4))):
+    for _ in range(0 if clean else int(rng.integers(1, 4))):
         p = int(rng.integers(lo, hi))
         f[p] ^= np.uint8(1 << int(rng.integers(0, 8)))
     try:
@@ -91,7 +98,9 @@ while time.time() - t0 < seconds:
         g_st, y = gpu(f, strategy, huff)
         counts["decodes"] += 1
         bad = None
-        if (o_st == "ok") != (g_st == "ok"):
+        if clean and g_st != "ok":
+            bad = f"clean file rejected: {g_st}"
+        elif (o_st == "ok") != (g_st == "ok"):
             bad = f"verdicts differ: oracle {o_st}, gpu {g_st}"
         elif g_st == "ok" and not np.array_equal(y, ref):
             bad = "both accept, outputs differ"
@@ -102,4 +111,5 @@ while time.time() - t0 < seconds:
                               "strategy": strategy, "huff": huff}), flush=True)
             sys.exit(1)
 counts["seconds"] = round(time.time() - t0, 1)
-print(json.dumps({"fuzz_campaign": "GPU fails iff the oracle fails, identical output otherwise", **counts}))
+print(json.dumps({"fuzz_campaign": ("clean files: GPU output == oracle output" if clean else
+                                   "GPU fails iff the oracle fails, identical output otherwise"), **counts}))
