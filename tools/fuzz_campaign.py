@@ -7,9 +7,10 @@ strategy that applies), and require the GPU to fail iff the oracle fails, with i
 Prints one JSON line of counts; exits non-zero on the first disagreement (after printing it).
 
 With --clean: no corruption, inputs up to 64 blocks of up to 1 MiB (full grids of every kernel variant), every
-output compared with the oracle's.
+output compared with the oracle's. With --clean --host: the same files through the end-to-end path
+(gomp_decompress_host: pinned host file -> chunked H2D / kernels / D2H pipeline -> host output).
 
-usage: python tools/fuzz_campaign.py [seconds] [seed] [--clean]
+usage: python tools/fuzz_campaign.py [seconds] [seed] [--clean [--host]]
 """
 import json
 import struct
@@ -26,7 +27,8 @@ import paper_1606_00519_b200 as gomp
 
 FORMAT_ERRORS = ("CORRUPT_STREAM", "MALFORMED_BACKREF", "HEADER_INCONSISTENT")
 clean = "--clean" in sys.argv
-argv = [v for v in sys.argv if v != "--clean"]
+host = "--host" in sys.argv
+argv = [v for v in sys.argv if v not in ("--clean", "--host")]
 seconds = float(argv[1]) if len(argv) > 1 else 300.0
 rng = np.random.default_rng(int(argv[2]) if len(argv) > 2 else 0)
 KINDS = ["wiki", "text", "matrix", "random", "zeros", "nested2", "nested8"]
@@ -42,6 +44,8 @@ def data(kind, n, seed):
 
 def gpu(f, strategy, huff):
     try:
+        if host:
+            return "ok", gomp.decompress_host(torch.as_tensor(f).pin_memory(), strategy=strategy).numpy().copy()
         y = gomp.decompress(torch.as_tensor(f).cuda(), strategy=strategy, huff=huff)
         return "ok", y.cpu().numpy()
     except gomp.GompError as e:
@@ -90,7 +94,9 @@ while time.time() - t0 < seconds:
     counts["oracle_ok" if o_st == "ok" else "oracle_err"] += 1
     runs = [("auto", None)]
     runs += [("mrr", None)] if de else [("sc", None)]
-    if mode == "bit":
+    if host:
+        pass
+    elif mode == "bit":
         runs += [("auto", "thread"), ("auto", "warp")]
     else:
         runs += [("de", None)]
@@ -111,5 +117,6 @@ while time.time() - t0 < seconds:
                               "strategy": strategy, "huff": huff}), flush=True)
             sys.exit(1)
 counts["seconds"] = round(time.time() - t0, 1)
-print(json.dumps({"fuzz_campaign": ("clean files: GPU output == oracle output" if clean else
+print(json.dumps({"fuzz_campaign": ("clean files through gomp_decompress_host: output == oracle output" if host else
+                                   "clean files: GPU output == oracle output" if clean else
                                    "GPU fails iff the oracle fails, identical output otherwise"), **counts}))
